@@ -1,0 +1,236 @@
+"""ctypes binding of oracle/_ref/libntf_ref.so (the compiled, unmodified reference).
+
+TEST INFRASTRUCTURE ONLY (see oracle/ntf_oracle.py header for who may import it).
+Build with ``make -C oracle`` (needs /root/reference; the built .so travels to
+the GPU box with the repo snapshot).  ``available()`` is False when the .so is
+absent; callers then fall back to the NumPy restatement.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_ref", "libntf_ref.so")
+_lib = None
+
+_P = C.POINTER(C.c_double)
+_U = C.POINTER(C.c_uint64)
+
+
+class RefError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+        self.msg = msg
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(LIB_PATH)
+        _lib.ntfref_last_error.restype = C.c_char_p
+    return _lib
+
+
+def _d(a: np.ndarray):
+    return a.ctypes.data_as(_P)
+
+
+def _u64(vals) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(vals, dtype=np.uint64))
+
+
+def _check(code):
+    if code != 0:
+        raise RefError(code, lib().ntfref_last_error().decode())
+
+
+def _cat(mats: Sequence[np.ndarray]) -> np.ndarray:
+    return np.ascontiguousarray(np.concatenate([np.asarray(m, dtype=np.float64).ravel() for m in mats]))
+
+
+def _split(flat: np.ndarray, shapes) -> List[np.ndarray]:
+    out, off = [], 0
+    for s in shapes:
+        n = int(np.prod(s))
+        out.append(flat[off:off + n].reshape(s).copy())
+        off += n
+    return out
+
+
+def cp_fit(algo: str, x: np.ndarray, init: Sequence[np.ndarray], beta, eps=1e-12, inner_steps=3,
+           max_iters=500, tol=0.0, extrapolate=False, extrap_cap=1.0, extrap_delta=1e-6):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    dims = _u64(x.shape)
+    rank = init[0].shape[1]
+    f = _cat(init)
+    tt = np.zeros(max_iters + 1)
+    tl = np.zeros(max_iters + 1)
+    n = C.c_int(0)
+    _check(lib().ntfref_cp_fit(C.c_int(0 if algo == "bcomm" else 1), C.c_int(x.ndim),
+                               dims.ctypes.data_as(_U), _d(x), C.c_int(rank), _d(f),
+                               C.c_double(beta), C.c_double(eps), C.c_int(inner_steps),
+                               C.c_int(max_iters), C.c_double(tol), C.c_int(int(extrapolate)),
+                               C.c_double(extrap_cap), C.c_double(extrap_delta), _d(tt), _d(tl),
+                               C.byref(n)))
+    return _split(f, [(d, rank) for d in x.shape]), tt[:n.value].copy(), tl[:n.value].copy()
+
+
+def tucker_fit(algo: str, x: np.ndarray, core: np.ndarray, factors: Sequence[np.ndarray], beta,
+               eps=1e-12, inner_steps=3, max_iters=500, tol=0.0, extrapolate=False,
+               extrap_cap=1.0, extrap_delta=1e-6):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    dims = _u64(x.shape)
+    ranks = _u64(core.shape)
+    c = np.ascontiguousarray(core, dtype=np.float64).copy()
+    f = _cat(factors)
+    tt = np.zeros(max_iters + 1)
+    tl = np.zeros(max_iters + 1)
+    n = C.c_int(0)
+    _check(lib().ntfref_tucker_fit(C.c_int(0 if algo == "bcomm" else 1), C.c_int(x.ndim),
+                                   dims.ctypes.data_as(_U), _d(x), ranks.ctypes.data_as(_U), _d(c),
+                                   _d(f), C.c_double(beta), C.c_double(eps), C.c_int(inner_steps),
+                                   C.c_int(max_iters), C.c_double(tol), C.c_int(int(extrapolate)),
+                                   C.c_double(extrap_cap), C.c_double(extrap_delta), _d(tt), _d(tl),
+                                   C.byref(n)))
+    return c, _split(f, list(zip(x.shape, core.shape))), tt[:n.value].copy(), tl[:n.value].copy()
+
+
+def cp_time_outer(algo: str, x: np.ndarray, init: Sequence[np.ndarray], beta, steps, inner_steps=5,
+                  eps=1e-12) -> Tuple[float, List[np.ndarray]]:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    dims = _u64(x.shape)
+    rank = init[0].shape[1]
+    f = _cat(init)
+    sec = C.c_double(0.0)
+    _check(lib().ntfref_cp_time_outer(C.c_int(0 if algo == "bcomm" else 1), C.c_int(x.ndim),
+                                      dims.ctypes.data_as(_U), _d(x), C.c_int(rank), _d(f),
+                                      C.c_double(beta), C.c_double(eps), C.c_int(inner_steps),
+                                      C.c_int(steps), C.byref(sec)))
+    return sec.value, _split(f, [(d, rank) for d in x.shape])
+
+
+def cp_block_update(x, factors, mode, beta, eps=1e-12, anchor: Optional[np.ndarray] = None):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    rank = factors[0].shape[1]
+    f = _cat(factors)
+    a = None if anchor is None else np.ascontiguousarray(anchor, dtype=np.float64)
+    _check(lib().ntfref_cp_block_update(C.c_int(x.ndim), _u64(x.shape).ctypes.data_as(_U), _d(x),
+                                        C.c_int(rank), _d(f), C.c_int(mode),
+                                        None if a is None else _d(a), C.c_double(beta), C.c_double(eps)))
+    return _split(f, [(d, rank) for d in x.shape])
+
+
+def cp_bcomm_sweep(x, factors, beta, eps=1e-12):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    rank = factors[0].shape[1]
+    f = _cat(factors)
+    _check(lib().ntfref_cp_bcomm_sweep(C.c_int(x.ndim), _u64(x.shape).ctypes.data_as(_U), _d(x),
+                                       C.c_int(rank), _d(f), C.c_double(beta), C.c_double(eps)))
+    return _split(f, [(d, rank) for d in x.shape])
+
+
+def cp_jcomm_reference(x, factors, beta, eps=1e-12):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    rank = factors[0].shape[1]
+    f = _cat(factors)
+    p = np.zeros_like(x)
+    q = np.zeros_like(x)
+    _check(lib().ntfref_cp_jcomm_reference(C.c_int(x.ndim), _u64(x.shape).ctypes.data_as(_U), _d(x),
+                                           C.c_int(rank), _d(f), C.c_double(beta), C.c_double(eps),
+                                           _d(p), _d(q)))
+    return p, q
+
+
+def cp_jcomm_inner_update(x, ref, current, mode, beta, eps=1e-12):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    rank = ref[0].shape[1]
+    r = _cat(ref)
+    c = _cat(current)
+    _check(lib().ntfref_cp_jcomm_inner_update(C.c_int(x.ndim), _u64(x.shape).ctypes.data_as(_U),
+                                              _d(x), C.c_int(rank), _d(r), _d(c), C.c_int(mode),
+                                              C.c_double(beta), C.c_double(eps)))
+    return _split(c, [(d, rank) for d in x.shape])
+
+
+def cp_jcomm_outer_step(x, factors, beta, inner_steps, eps=1e-12):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    rank = factors[0].shape[1]
+    f = _cat(factors)
+    _check(lib().ntfref_cp_jcomm_outer_step(C.c_int(x.ndim), _u64(x.shape).ctypes.data_as(_U), _d(x),
+                                            C.c_int(rank), _d(f), C.c_double(beta),
+                                            C.c_int(inner_steps), C.c_double(eps)))
+    return _split(f, [(d, rank) for d in x.shape])
+
+
+def cp_reconstruct(factors):
+    dims = [a.shape[0] for a in factors]
+    rank = factors[0].shape[1]
+    out = np.zeros(dims)
+    _check(lib().ntfref_cp_reconstruct(C.c_int(len(dims)), _u64(dims).ctypes.data_as(_U), C.c_int(rank),
+                                       _d(_cat(factors)), _d(out)))
+    return out
+
+
+def cp_contract(t, factors, mode):
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    rank = factors[mode].shape[1]
+    out = np.zeros((t.shape[mode], rank))
+    _check(lib().ntfref_cp_contract(C.c_int(t.ndim), _u64(t.shape).ctypes.data_as(_U), _d(t),
+                                    C.c_int(rank), _d(_cat(factors)), C.c_int(mode), _d(out)))
+    return out
+
+
+def D_beta(x, xhat, beta):
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    xh = np.ascontiguousarray(xhat, dtype=np.float64).ravel()
+    out = C.c_double(0)
+    _check(lib().ntfref_D_beta(C.c_uint64(x.size), _d(x), _d(xh), C.c_double(beta), C.byref(out)))
+    return out.value
+
+
+def tucker_reconstruct(core, factors):
+    dims = [a.shape[0] for a in factors]
+    out = np.zeros(dims)
+    c = np.ascontiguousarray(core, dtype=np.float64)
+    _check(lib().ntfref_tucker_reconstruct(C.c_int(len(dims)), _u64(dims).ctypes.data_as(_U),
+                                           _u64(core.shape).ctypes.data_as(_U), _d(c),
+                                           _d(_cat(factors)), _d(out)))
+    return out
+
+
+def tucker_step(kind, x, core, factors, mode=0, beta=1.0, inner=1, eps=1e-12, ref=None):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    c = np.ascontiguousarray(core, dtype=np.float64).copy()
+    f = _cat(factors)
+    rc = rf = None
+    if ref is not None:
+        rc = np.ascontiguousarray(ref[0], dtype=np.float64)
+        rf = _cat(ref[1])
+    _check(lib().ntfref_tucker_step(C.c_int(kind), C.c_int(x.ndim), _u64(x.shape).ctypes.data_as(_U),
+                                    _d(x), _u64(core.shape).ctypes.data_as(_U),
+                                    None if rc is None else _d(rc), None if rf is None else _d(rf),
+                                    _d(c), _d(f), C.c_int(mode), C.c_double(beta), C.c_int(inner),
+                                    C.c_double(eps)))
+    return c, _split(f, list(zip(x.shape, core.shape)))
+
+
+def rng_uniform(seed, stream, n):
+    out = np.zeros(n)
+    _check(lib().ntfref_rng_uniform(C.c_uint64(seed), C.c_uint64(stream), C.c_uint64(n), _d(out)))
+    return out
+
+
+def init_cp_factors(dims, rank, seed, eps=1e-12):
+    out = np.zeros(int(sum(dims)) * rank)
+    _check(lib().ntfref_init_cp_factors(C.c_int(len(dims)), _u64(dims).ctypes.data_as(_U), C.c_int(rank),
+                                        C.c_uint64(seed), C.c_double(eps), _d(out)))
+    return _split(out, [(d, rank) for d in dims])
