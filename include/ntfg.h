@@ -1,0 +1,211 @@
+/*
+ * ntfg.h -- C ABI of the B200 beta-divergence MU engine (libntfg.so).
+ *
+ * This is the drop-in boundary: plain pointers, sizes and status codes, no
+ * C++ or torch types.  Each entry point replaces one reference interface of
+ * /root/reference/proj (cited per function).  The C++ drop-in API
+ * (include/ntf/ntf.hpp, namespace ntf) is a thin layer over these calls; the
+ * Python package binds them with ctypes.
+ *
+ * Conventions
+ *  - Tensors are row-major (last index fastest) with uint64 dims, as the
+ *    reference DenseTensor (include/ntf/tensor.hpp:20-53).
+ *  - CP factors are passed as ONE host fp64 buffer: the row-major I_n x R
+ *    blocks concatenated in mode order (reference CpFactors, cp.hpp:13-22).
+ *  - Tucker: core row-major (J_0..J_{N-1}) plus concatenated I_n x J_n
+ *    factor blocks (reference TuckerModel, tucker.hpp:14-24).
+ *  - No exception crosses this boundary; failures return a status and
+ *    ntfg_last_error() holds the message (thread-local).
+ */
+#ifndef NTFG_H_
+#define NTFG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NTFG_ABI_VERSION 1
+
+/* Status codes; the C++ layer maps them onto the reference exception
+ * hierarchy (include/ntf/errors.hpp:10-43). */
+typedef enum ntfg_status {
+  NTFG_OK = 0,
+  NTFG_ERR_SHAPE = 1,     /* ntf::ShapeError     */
+  NTFG_ERR_DOMAIN = 2,    /* ntf::DomainError    */
+  NTFG_ERR_NUMERICAL = 3, /* ntf::NumericalError */
+  NTFG_ERR_FORMAT = 4,    /* ntf::FormatError    */
+  NTFG_ERR_CUDA = 5,
+  NTFG_ERR_COMM = 6,
+  NTFG_ERR_OOM = 7,
+  NTFG_ERR_INTERNAL = 8
+} ntfg_status;
+
+typedef enum ntfg_precision { NTFG_F64 = 0, NTFG_F32 = 1 } ntfg_precision;
+typedef enum ntfg_algo { NTFG_BCOMM = 0, NTFG_JCOMM = 1 } ntfg_algo;
+typedef enum ntfg_location { NTFG_HOST = 0, NTFG_DEVICE = 1 } ntfg_location;
+
+typedef struct ntfg_context ntfg_context;
+
+/* Optional collective hook for data-parallel (mode-0 slab) fits: sums
+ * `count` doubles at `device_buf` across ranks, in place, ordered on
+ * `cuda_stream`.  Return 0 on success. */
+typedef int (*ntfg_allreduce_fn)(void* user, double* device_buf, size_t count, void* cuda_stream);
+
+/* Mirrors ntf::FitConfig (reference include/ntf/config.hpp:24-39) plus the
+ * device options the north star adds as NEW fields (precision, graphs). */
+typedef struct ntfg_fit_config {
+  double beta;
+  uint64_t rank;          /* CP rank */
+  const uint64_t* ranks;  /* Tucker core shape (n_ranks entries) */
+  uint32_t n_ranks;
+  double eps;
+  uint64_t inner_steps;
+  uint64_t max_iters;
+  double tol;
+  uint64_t seed;
+  int32_t extrapolate;
+  double extrap_cap;
+  double extrap_delta;
+  int32_t has_data_floor;
+  double data_floor;
+  int32_t precision;      /* ntfg_precision: streaming type (fp64 validation / fp32) */
+  int32_t use_graphs;     /* capture the outer iteration in a CUDA graph */
+} ntfg_fit_config;
+
+/* reference TraceRecord (config.hpp:18-22) */
+typedef struct ntfg_trace_row {
+  uint64_t iter;
+  double time_s;
+  double loss;
+} ntfg_trace_row;
+
+/* Data-parallel slab placement of this rank's X: rows [slab_begin,
+ * slab_begin + dims[0]) of a tensor whose mode-0 extent is global_dim0. */
+typedef struct ntfg_shard {
+  uint64_t global_dim0;
+  uint64_t slab_begin;
+} ntfg_shard;
+
+typedef struct ntfg_stats {
+  uint64_t kernel_launches;   /* kernels enqueued by the last call (graph nodes counted per replay) */
+  uint64_t graph_launches;
+  double device_ms;           /* device time of the last fit's timed steps */
+  double objective_ms;        /* device time of standalone objective passes */
+} ntfg_stats;
+
+/* ---- context ------------------------------------------------------------- */
+int ntfg_abi_version(void);
+const char* ntfg_last_error(void);
+ntfg_status ntfg_context_create(int device, ntfg_context** out);
+ntfg_status ntfg_context_destroy(ntfg_context* ctx);
+ntfg_status ntfg_context_set_stream(ntfg_context* ctx, void* cuda_stream);
+ntfg_status ntfg_context_set_allreduce(ntfg_context* ctx, ntfg_allreduce_fn fn, void* user);
+ntfg_status ntfg_context_stats(const ntfg_context* ctx, ntfg_stats* out);
+/* Release cached device buffers. */
+ntfg_status ntfg_context_trim(ntfg_context* ctx);
+
+/* validate_fit_config (reference config.hpp:43, config.cpp:7-18) */
+ntfg_status ntfg_validate_fit_config(const ntfg_fit_config* cfg);
+
+/* ---- fit drivers ------------------------------------------------------------
+ * x: `order` dims, dtype 0 = fp64, 1 = fp32, on host or device (location).
+ * trace: capacity max_iters + 1 rows; *trace_len receives the row count.
+ * shard: NULL for a single-device fit. */
+
+/* bcomm_fit / jcomm_fit (reference cp.hpp:48,76; cp.cpp:244-298) */
+ntfg_status ntfg_cp_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t algo,
+                        uint32_t order, const uint64_t* dims, const void* x, int32_t x_dtype,
+                        int32_t x_location, const ntfg_shard* shard, double* factors_inout,
+                        ntfg_trace_row* trace, uint64_t* trace_len);
+
+/* tucker_bcomm_fit / tucker_jcomm_fit (reference tucker.hpp:55,84; tucker.cpp:221-275) */
+ntfg_status ntfg_tucker_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t algo,
+                            uint32_t order, const uint64_t* dims, const void* x, int32_t x_dtype,
+                            int32_t x_location, const ntfg_shard* shard, double* core_inout,
+                            double* factors_inout, ntfg_trace_row* trace, uint64_t* trace_len);
+
+/* ---- CP step level (host fp64 buffers; device round trip per call) ------------ */
+
+/* cp_reconstruct (reference cp.hpp:30, cp.cpp:26-76) */
+ntfg_status ntfg_cp_reconstruct(ntfg_context* ctx, int32_t precision, uint32_t order,
+                                const uint64_t* dims, uint64_t rank, const double* factors,
+                                double* out);
+/* cp_contract (reference tensor.hpp:105, tensor.cpp:372-406) */
+ntfg_status ntfg_cp_contract(ntfg_context* ctx, int32_t precision, uint32_t order,
+                             const uint64_t* dims, const double* t, uint64_t rank,
+                             const double* factors, uint32_t mode, double* out);
+/* D_beta_mean(x, cp_reconstruct(f)) fused (reference cp.cpp:264,293) */
+ntfg_status ntfg_cp_objective(ntfg_context* ctx, int32_t precision, double beta, uint32_t order,
+                              const uint64_t* dims, const double* x, uint64_t rank,
+                              const double* factors, double* mean_out);
+/* cp_block_update_anchored / bcomm_block_update (reference cp.hpp:37-45, cp.cpp:109-129);
+ * anchor NULL => bcomm_block_update.  Updates block `mode` of factors_inout. */
+ntfg_status ntfg_cp_block_update(ntfg_context* ctx, int32_t precision, double beta, double eps,
+                                 uint32_t order, const uint64_t* dims, const double* x,
+                                 uint64_t rank, double* factors_inout, uint32_t mode,
+                                 const double* anchor);
+/* bcomm_sweep (reference cp.hpp:47, cp.cpp:131-135) */
+ntfg_status ntfg_cp_bcomm_sweep(ntfg_context* ctx, int32_t precision, double beta, double eps,
+                                uint32_t order, const uint64_t* dims, const double* x,
+                                uint64_t rank, double* factors_inout);
+/* make_jcomm_reference (reference cp.hpp:61, cp.cpp:202-208): host P~, Q~ out */
+ntfg_status ntfg_cp_jcomm_reference(ntfg_context* ctx, int32_t precision, double beta,
+                                    double eps, uint32_t order, const uint64_t* dims,
+                                    const double* x, uint64_t rank, const double* factors,
+                                    double* p_out, double* q_out);
+/* jcomm_inner_update (reference cp.hpp:68, cp.cpp:210-229) from cached host P~, Q~ */
+ntfg_status ntfg_cp_jcomm_inner_update(ntfg_context* ctx, int32_t precision, double beta,
+                                       double eps, uint32_t order, const uint64_t* dims,
+                                       const double* p, const double* q, uint64_t rank,
+                                       const double* ref_factors, double* current_inout,
+                                       uint32_t mode);
+/* jcomm_outer_step (reference cp.hpp:73, cp.cpp:231-240) */
+ntfg_status ntfg_cp_jcomm_outer_step(ntfg_context* ctx, int32_t precision, double beta,
+                                     double eps, uint64_t inner_steps, uint32_t order,
+                                     const uint64_t* dims, const double* x, uint64_t rank,
+                                     double* factors_inout);
+
+/* ---- divergence on explicit arrays ---------------------------------------------- */
+/* D_beta (reference divergence.hpp:30, divergence.cpp:35-40) */
+ntfg_status ntfg_D_beta(ntfg_context* ctx, double beta, uint64_t n, const double* x,
+                        const double* xhat, double* out);
+
+/* ---- Tucker step level -------------------------------------------------------------- */
+/* tucker_reconstruct (reference tensor.hpp:109, tensor.cpp:408-419) */
+ntfg_status ntfg_tucker_reconstruct(ntfg_context* ctx, int32_t precision, uint32_t order,
+                                    const uint64_t* dims, const uint64_t* ranks,
+                                    const double* core, const double* factors, double* out);
+/* tucker_multimode_contract (reference tensor.hpp:116, tensor.cpp:421-456);
+ * cols[n] = factor n column count; skip < 0 => none */
+ntfg_status ntfg_tucker_multimode_contract(ntfg_context* ctx, int32_t precision, uint32_t order,
+                                           const uint64_t* dims, const double* t,
+                                           const uint64_t* cols, const double* factors,
+                                           int32_t skip, double* out);
+/* tucker_factor_contract (reference tensor.hpp:128, tensor.cpp:514-560) */
+ntfg_status ntfg_tucker_factor_contract(ntfg_context* ctx, int32_t precision, uint32_t order,
+                                        const uint64_t* dims, const double* t,
+                                        const uint64_t* ranks, const double* core,
+                                        const double* factors, uint32_t mode, double* out);
+/* D_beta_mean(x, tucker_reconstruct(m)) (reference tucker.cpp:242,270) */
+ntfg_status ntfg_tucker_objective(ntfg_context* ctx, int32_t precision, double beta,
+                                  uint32_t order, const uint64_t* dims, const double* x,
+                                  const uint64_t* ranks, const double* core,
+                                  const double* factors, double* mean_out);
+/* Tucker step kinds (reference tucker.hpp:38-82):
+ *  0 block_core_update, 1 block_factor_update(mode), 2 tucker_bcomm_sweep,
+ *  3 jcomm_tucker_outer_step(inner_steps),
+ *  4 jcomm_inner_core_update and 5 jcomm_inner_factor_update(mode) against the
+ *    reference model (ref_core, ref_factors) whose P~/Q~ are built from x. */
+ntfg_status ntfg_tucker_step(ntfg_context* ctx, int32_t precision, int32_t kind, double beta,
+                             double eps, uint64_t inner_steps, uint32_t order,
+                             const uint64_t* dims, const double* x, const uint64_t* ranks,
+                             const double* ref_core, const double* ref_factors,
+                             double* core_inout, double* factors_inout, uint32_t mode);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NTFG_H_ */

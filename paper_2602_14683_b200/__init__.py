@@ -1,0 +1,18 @@
+"""B200-native contraction-only beta-divergence MU engine (CP / Tucker, B-CoMM / J-CoMM).
+
+The compute path is libntfg.so (hand-written sm_100a CUDA kernels behind the C
+ABI in include/ntfg.h); this package is the Python mirror of the reference's
+``ntf`` solver API on top of it.  See DESIGN.md.
+"""
+from .api import (  # noqa: F401
+    CommError, Context, CpFitResult, CudaError, D_beta, D_beta_mean, DomainError, FitConfig,
+    FormatError, JcommCpReference, JcommTuckerReference, NtfError, NumericalError, ShapeError,
+    TraceRecord, TuckerFitResult, bcomm_block_update, bcomm_fit, bcomm_sweep, block_core_update,
+    block_factor_update, cp_block_update_anchored, cp_contract, cp_objective, cp_reconstruct,
+    default_context, jcomm_fit, jcomm_inner_core_update, jcomm_inner_factor_update,
+    jcomm_inner_update, jcomm_outer_step, jcomm_tucker_outer_step, make_jcomm_reference,
+    make_jcomm_tucker_reference, tucker_bcomm_fit, tucker_bcomm_sweep, tucker_factor_contract,
+    tucker_jcomm_fit, tucker_multimode_contract, tucker_objective, tucker_reconstruct,
+    validate_fit_config)
+
+__version__ = "0.1.0"

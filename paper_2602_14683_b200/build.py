@@ -1,0 +1,84 @@
+"""In-tree build of the native libraries (sm_100a only).
+
+  libntfg.so      C ABI + CUDA kernels (include/ntfg.h)
+  libntf_b200.so  drop-in C++ API, namespace ntf (include/ntf/ntf.hpp),
+                  a thin layer over libntfg.so
+
+Both land in paper_2602_14683_b200/lib/ (git-ignored, shipped to the GPU box
+with the repo snapshot).  Objects are rebuilt only when a source or header is
+newer than the object.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "lib")
+OBJ = os.path.join(PKG, "lib", "obj")
+INCLUDE = os.path.join(ROOT, "include")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                  "-Xcompiler", "-fvisibility=hidden", "-I" + INCLUDE, "-I" + CSRC]
+CU_SOURCES = ["cp_api.cu", "tucker_api.cu", "capi.cu"]
+CXX_API_SOURCES = ["ntf_api.cpp"]
+
+
+def _headers():
+    hs = []
+    for d in (CSRC, INCLUDE, os.path.join(INCLUDE, "ntf")):
+        if os.path.isdir(d):
+            hs += [os.path.join(d, f) for f in os.listdir(d) if f.endswith((".cuh", ".h", ".hpp"))]
+    return hs
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("build failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+    return r
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    hdrs = _headers()
+    jobs = []
+    objs = []
+    for src in CU_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        objs.append(o)
+        if force or _stale(o, [s] + hdrs):
+            jobs.append([NVCC] + NVFLAGS + ["-c", s, "-o", o])
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
+        for r in ex.map(_run, jobs):
+            if verbose and (r.stdout or r.stderr):
+                print(r.stdout + r.stderr, file=sys.stderr)
+    lib = os.path.join(LIB, "libntfg.so")
+    if force or jobs or _stale(lib, objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcuda"])
+    # drop-in C++ API over the C ABI
+    api_srcs = [os.path.join(CSRC, s) for s in CXX_API_SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    if api_srcs:
+        lib2 = os.path.join(LIB, "libntf_b200.so")
+        if force or _stale(lib2, api_srcs + hdrs + [lib]):
+            _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I" + INCLUDE, "-o", lib2] + api_srcs
+                 + ["-L" + LIB, "-lntfg", "-Wl,-rpath,$ORIGIN"])
+    return lib
+
+
+if __name__ == "__main__":
+    print(build(verbose=True, force="--force" in sys.argv))

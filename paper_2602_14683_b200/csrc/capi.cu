@@ -1,0 +1,325 @@
+// extern "C" boundary of libntfg.so (declared in include/ntfg.h).  Converts
+// internal exceptions into status codes + a thread-local message; no C++
+// exception crosses this boundary.
+#include <cstdio>
+#include <string>
+
+#include "engine.cuh"
+
+namespace ntfg {
+// cp_api.cu
+void cp_fit(Context&, const ntfg_fit_config&, int, uint32_t, const uint64_t*, const void*, int, int,
+            const ntfg_shard*, double*, ntfg_trace_row*, uint64_t*);
+void cp_reconstruct(Context&, int, uint32_t, const uint64_t*, uint64_t, const double*, double*);
+void cp_contract(Context&, int, uint32_t, const uint64_t*, const double*, uint64_t, const double*,
+                 uint32_t, double*);
+void cp_objective(Context&, int, double, uint32_t, const uint64_t*, const double*, uint64_t,
+                  const double*, double*);
+void cp_block_update(Context&, int, double, double, uint32_t, const uint64_t*, const double*,
+                     uint64_t, double*, uint32_t, const double*);
+void cp_bcomm_sweep(Context&, int, double, double, uint32_t, const uint64_t*, const double*,
+                    uint64_t, double*);
+void cp_jcomm_reference(Context&, int, double, double, uint32_t, const uint64_t*, const double*,
+                        uint64_t, const double*, double*, double*);
+void cp_jcomm_inner_update(Context&, int, double, double, uint32_t, const uint64_t*, const double*,
+                           const double*, uint64_t, const double*, double*, uint32_t);
+void cp_jcomm_outer_step(Context&, int, double, double, uint64_t, uint32_t, const uint64_t*,
+                         const double*, uint64_t, double*);
+void D_beta(Context&, double, uint64_t, const double*, const double*, double*);
+// tucker_api.cu
+void tucker_fit(Context&, const ntfg_fit_config&, int, uint32_t, const uint64_t*, const void*, int,
+                int, const ntfg_shard*, double*, double*, ntfg_trace_row*, uint64_t*);
+void tucker_reconstruct(Context&, int, uint32_t, const uint64_t*, const uint64_t*, const double*,
+                        const double*, double*);
+void tucker_multimode_contract(Context&, int, uint32_t, const uint64_t*, const double*,
+                               const uint64_t*, const double*, int32_t, double*);
+void tucker_factor_contract(Context&, int, uint32_t, const uint64_t*, const double*,
+                            const uint64_t*, const double*, const double*, uint32_t, double*);
+void tucker_objective(Context&, int, double, uint32_t, const uint64_t*, const double*,
+                      const uint64_t*, const double*, const double*, double*);
+void tucker_step(Context&, int, int, double, double, uint64_t, uint32_t, const uint64_t*,
+                 const double*, const uint64_t*, const double*, const double*, double*, double*,
+                 uint32_t);
+}  // namespace ntfg
+
+struct ntfg_context : ntfg::Context {};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+ntfg_status guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return NTFG_OK;
+  } catch (const ntfg::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return NTFG_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return NTFG_ERR_INTERNAL;
+  }
+}
+
+template <class F>
+ntfg_status with_ctx(ntfg_context* ctx, F&& f) {
+  if (!ctx) {
+    g_last_error = "null context";
+    return NTFG_ERR_INTERNAL;
+  }
+  return guard([&] {
+    ctx->activate();
+    f(*ctx);
+  });
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw ntfg::Error(NTFG_ERR_SHAPE, std::string(what) + " must not be NULL");
+}
+}  // namespace
+
+#define NTFG_API extern "C" __attribute__((visibility("default")))
+
+NTFG_API int ntfg_abi_version(void) { return NTFG_ABI_VERSION; }
+NTFG_API const char* ntfg_last_error(void) { return g_last_error.c_str(); }
+
+NTFG_API ntfg_status ntfg_context_create(int device, ntfg_context** out) {
+  return guard([&] {
+    need(out, "out");
+    int n = 0;
+    ntfg::cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) throw ntfg::Error(NTFG_ERR_CUDA, "no such CUDA device");
+    auto* c = new ntfg_context();
+    c->device = device;
+    try {
+      c->activate();
+      ntfg::cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      c->own_stream = true;
+      cudaDeviceProp prop;
+      ntfg::cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+      c->sm_count = prop.multiProcessorCount;
+      if (prop.major < 10)
+        throw ntfg::Error(NTFG_ERR_CUDA, "libntfg is built for sm_100a (B200); device is sm_" +
+                                             std::to_string(prop.major) + std::to_string(prop.minor));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+NTFG_API ntfg_status ntfg_context_destroy(ntfg_context* ctx) {
+  if (!ctx) return NTFG_OK;
+  return guard([&] {
+    ctx->activate();
+    cudaStreamSynchronize(ctx->stream);
+    ctx->bufs.release();
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+NTFG_API ntfg_status ntfg_context_set_stream(ntfg_context* ctx, void* stream) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    if (c.own_stream) cudaStreamDestroy(c.stream);
+    c.stream = static_cast<cudaStream_t>(stream);
+    c.own_stream = false;
+  });
+}
+
+NTFG_API ntfg_status ntfg_context_set_allreduce(ntfg_context* ctx, ntfg_allreduce_fn fn, void* user) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    c.allreduce = fn;
+    c.allreduce_user = user;
+  });
+}
+
+NTFG_API ntfg_status ntfg_context_stats(const ntfg_context* ctx, ntfg_stats* out) {
+  if (!ctx || !out) return NTFG_ERR_INTERNAL;
+  *out = ctx->stats;
+  return NTFG_OK;
+}
+
+NTFG_API ntfg_status ntfg_context_trim(ntfg_context* ctx) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    c.sync();
+    c.bufs.release();
+  });
+}
+
+NTFG_API ntfg_status ntfg_validate_fit_config(const ntfg_fit_config* cfg) {
+  return guard([&] {
+    need(cfg, "cfg");
+    ntfg::validate_config(*cfg);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t algo,
+                                 uint32_t order, const uint64_t* dims, const void* x,
+                                 int32_t x_dtype, int32_t x_location, const ntfg_shard* shard,
+                                 double* factors, ntfg_trace_row* trace, uint64_t* trace_len) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(cfg, "cfg"); need(dims, "dims"); need(x, "x"); need(factors, "factors");
+    need(trace, "trace"); need(trace_len, "trace_len");
+    ntfg::cp_fit(c, *cfg, algo, order, dims, x, x_dtype, x_location, shard, factors, trace, trace_len);
+  });
+}
+
+NTFG_API ntfg_status ntfg_tucker_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t algo,
+                                     uint32_t order, const uint64_t* dims, const void* x,
+                                     int32_t x_dtype, int32_t x_location, const ntfg_shard* shard,
+                                     double* core, double* factors, ntfg_trace_row* trace,
+                                     uint64_t* trace_len) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(cfg, "cfg"); need(dims, "dims"); need(x, "x"); need(core, "core");
+    need(factors, "factors"); need(trace, "trace"); need(trace_len, "trace_len");
+    ntfg::tucker_fit(c, *cfg, algo, order, dims, x, x_dtype, x_location, shard, core, factors,
+                     trace, trace_len);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_reconstruct(ntfg_context* ctx, int32_t precision, uint32_t order,
+                                         const uint64_t* dims, uint64_t rank,
+                                         const double* factors, double* out) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(factors, "factors"); need(out, "out");
+    ntfg::cp_reconstruct(c, precision, order, dims, rank, factors, out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_contract(ntfg_context* ctx, int32_t precision, uint32_t order,
+                                      const uint64_t* dims, const double* t, uint64_t rank,
+                                      const double* factors, uint32_t mode, double* out) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(t, "t"); need(factors, "factors"); need(out, "out");
+    ntfg::cp_contract(c, precision, order, dims, t, rank, factors, mode, out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_objective(ntfg_context* ctx, int32_t precision, double beta,
+                                       uint32_t order, const uint64_t* dims, const double* x,
+                                       uint64_t rank, const double* factors, double* mean_out) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(x, "x"); need(factors, "factors"); need(mean_out, "mean_out");
+    ntfg::cp_objective(c, precision, beta, order, dims, x, rank, factors, mean_out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_block_update(ntfg_context* ctx, int32_t precision, double beta,
+                                          double eps, uint32_t order, const uint64_t* dims,
+                                          const double* x, uint64_t rank, double* factors,
+                                          uint32_t mode, const double* anchor) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(x, "x"); need(factors, "factors");
+    ntfg::cp_block_update(c, precision, beta, eps, order, dims, x, rank, factors, mode, anchor);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_bcomm_sweep(ntfg_context* ctx, int32_t precision, double beta,
+                                         double eps, uint32_t order, const uint64_t* dims,
+                                         const double* x, uint64_t rank, double* factors) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(x, "x"); need(factors, "factors");
+    ntfg::cp_bcomm_sweep(c, precision, beta, eps, order, dims, x, rank, factors);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_jcomm_reference(ntfg_context* ctx, int32_t precision, double beta,
+                                             double eps, uint32_t order, const uint64_t* dims,
+                                             const double* x, uint64_t rank, const double* factors,
+                                             double* p_out, double* q_out) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(x, "x"); need(factors, "factors"); need(p_out, "p_out"); need(q_out, "q_out");
+    ntfg::cp_jcomm_reference(c, precision, beta, eps, order, dims, x, rank, factors, p_out, q_out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_jcomm_inner_update(ntfg_context* ctx, int32_t precision, double beta,
+                                                double eps, uint32_t order, const uint64_t* dims,
+                                                const double* p, const double* q, uint64_t rank,
+                                                const double* ref, double* current, uint32_t mode) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(p, "p"); need(q, "q"); need(ref, "ref"); need(current, "current");
+    ntfg::cp_jcomm_inner_update(c, precision, beta, eps, order, dims, p, q, rank, ref, current, mode);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_jcomm_outer_step(ntfg_context* ctx, int32_t precision, double beta,
+                                              double eps, uint64_t inner_steps, uint32_t order,
+                                              const uint64_t* dims, const double* x, uint64_t rank,
+                                              double* factors) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(x, "x"); need(factors, "factors");
+    ntfg::cp_jcomm_outer_step(c, precision, beta, eps, inner_steps, order, dims, x, rank, factors);
+  });
+}
+
+NTFG_API ntfg_status ntfg_D_beta(ntfg_context* ctx, double beta, uint64_t n, const double* x,
+                                 const double* xhat, double* out) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(out, "out");
+    ntfg::D_beta(c, beta, n, x, xhat, out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_tucker_reconstruct(ntfg_context* ctx, int32_t precision, uint32_t order,
+                                             const uint64_t* dims, const uint64_t* ranks,
+                                             const double* core, const double* factors,
+                                             double* out) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(ranks, "ranks"); need(core, "core"); need(factors, "factors"); need(out, "out");
+    ntfg::tucker_reconstruct(c, precision, order, dims, ranks, core, factors, out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_tucker_multimode_contract(ntfg_context* ctx, int32_t precision,
+                                                    uint32_t order, const uint64_t* dims,
+                                                    const double* t, const uint64_t* cols,
+                                                    const double* factors, int32_t skip,
+                                                    double* out) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(t, "t"); need(cols, "cols"); need(factors, "factors"); need(out, "out");
+    ntfg::tucker_multimode_contract(c, precision, order, dims, t, cols, factors, skip, out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_tucker_factor_contract(ntfg_context* ctx, int32_t precision,
+                                                 uint32_t order, const uint64_t* dims,
+                                                 const double* t, const uint64_t* ranks,
+                                                 const double* core, const double* factors,
+                                                 uint32_t mode, double* out) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(t, "t"); need(ranks, "ranks"); need(core, "core");
+    need(factors, "factors"); need(out, "out");
+    ntfg::tucker_factor_contract(c, precision, order, dims, t, ranks, core, factors, mode, out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_tucker_objective(ntfg_context* ctx, int32_t precision, double beta,
+                                           uint32_t order, const uint64_t* dims, const double* x,
+                                           const uint64_t* ranks, const double* core,
+                                           const double* factors, double* mean_out) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(x, "x"); need(ranks, "ranks"); need(core, "core");
+    need(factors, "factors"); need(mean_out, "mean_out");
+    ntfg::tucker_objective(c, precision, beta, order, dims, x, ranks, core, factors, mean_out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_tucker_step(ntfg_context* ctx, int32_t precision, int32_t kind,
+                                      double beta, double eps, uint64_t inner_steps,
+                                      uint32_t order, const uint64_t* dims, const double* x,
+                                      const uint64_t* ranks, const double* ref_core,
+                                      const double* ref_factors, double* core, double* factors,
+                                      uint32_t mode) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(x, "x"); need(ranks, "ranks"); need(core, "core"); need(factors, "factors");
+    ntfg::tucker_step(c, precision, kind, beta, eps, inner_steps, order, dims, x, ranks, ref_core,
+                      ref_factors, core, factors, mode);
+  });
+}

@@ -1,0 +1,513 @@
+// CP engine: device state of one CP problem and the B-CoMM / J-CoMM steps.
+//
+// Reference call stacks:
+//   bcomm_block_update  cp.cpp:109-129  = recon(P,Q) -> contract -> finalize
+//   make_jcomm_reference cp.cpp:202-208 = recon(P~,Q~) (+ fused objective)
+//   jcomm_inner_update  cp.cpp:210-229  = contract(P~ chi1, Q~ chi2) -> finalize
+// The whole outer iteration is enqueued on one stream and (optionally)
+// captured once into a CUDA graph by the fit driver.
+#pragma once
+#include <algorithm>
+#include <vector>
+
+#include "cp_kernels.cuh"
+#include "engine.cuh"
+
+namespace ntfg {
+
+template <typename T>
+class CpEngine {
+ public:
+  // dims: this rank's extents (dims[0] = slab rows when sharded).
+  CpEngine(Context& c, uint32_t order, const uint64_t* dims, int64_t rank, double beta,
+           double eps, const ntfg_shard* shard)
+      : c_(c), N_(int(order)), R_(rank), beta_(beta), eps_(eps) {
+    if (order < 1 || order > uint32_t(kMaxOrder))
+      throw Error(NTFG_ERR_SHAPE, "tensor order must be in [1, 8]");
+    if (rank < 1) throw Error(NTFG_ERR_DOMAIN, "rank must be >= 1");
+    RP_ = pad_rank(rank);
+    gamma_ = gamma_of(beta);
+    bk_ = beta_kind_of(beta);
+    g_.order = N_;
+    E_ = 1;
+    for (int m = 0; m < N_; ++m) {
+      if (dims[m] < 1) throw Error(NTFG_ERR_SHAPE, "tensor dimensions must be >= 1");
+      g_.dims[m] = int64_t(dims[m]);
+      E_ *= g_.dims[m];
+    }
+    g_.K = g_.dims[N_ - 1];
+    g_.rows = E_ / g_.K;
+    int64_t st = 1;
+    for (int m = N_ - 2; m >= 0; --m) {
+      g_.rstride[m] = st;
+      st *= g_.dims[m];
+    }
+    E_global_ = E_;
+    if (shard) {
+      if (shard->slab_begin + dims[0] > shard->global_dim0)
+        throw Error(NTFG_ERR_SHAPE, "shard slab exceeds the global mode-0 extent");
+      E_global_ = E_ / g_.dims[0] * int64_t(shard->global_dim0);
+      sharded_ = c_.allreduce != nullptr;
+    }
+    off_.resize(N_ + 1, 0);
+    for (int m = 0; m < N_; ++m) off_[m + 1] = off_[m] + g_.dims[m] * R_;
+    const size_t F = size_t(off_[N_]);
+    A_ = c_.buf<double>("cp.A", F);
+    Aref_ = c_.buf<double>("cp.Aref", F);
+    chi1_ = c_.buf<double>("cp.chi1", F);
+    chi2_ = c_.buf<double>("cp.chi2", F);
+    anch_ = c_.buf<double>("cp.anchor", F);
+    stage_ = c_.buf<T>("cp.stage", size_t(g_.K) * RP_);
+    stage_anchor_ = c_.buf<T>("cp.stage_anchor", size_t(g_.K) * RP_);
+    colsum_ = c_.buf<double>("cp.colsum", size_t(N_) * R_ + 1);
+    colprod_ = c_.buf<double>("cp.colprod", size_t(R_));
+    flags_ = c_.buf<unsigned>("cp.flags", 1);
+    counter_ = c_.buf<int>("cp.counter", 1);
+    raw_ = c_.buf<double>("cp.raw", 1);
+    numden_ = c_.buf<double>("cp.numden", size_t(2) * max_dim() * R_);
+    // objective partial count = recon grid
+    recon_grid_ = int(std::min<int64_t>(recon_work(), int64_t(c_.sm_count) * 4));
+    objpart_ = c_.buf<double>("cp.objpart", size_t(recon_grid_));
+  }
+
+  int order() const { return N_; }
+  int64_t entries() const { return E_; }
+  int64_t entries_global() const { return E_global_; }
+  int64_t dim(int m) const { return g_.dims[m]; }
+  size_t factor_doubles() const { return size_t(off_[N_]); }
+  double* A(int m) const { return A_ + off_[m]; }
+  double* A_all() const { return A_; }
+
+  // ---- data & parameters ---------------------------------------------------
+  void set_x(const void* x, int dtype, int location) {
+    const bool want_f32 = sizeof(T) == 4;
+    if (location == NTFG_DEVICE && ((dtype == 1) == want_f32)) {
+      x_ = static_cast<const T*>(x);
+      return;
+    }
+    T* dst = c_.buf<T>("cp.x", size_t(E_));
+    upload_convert(dst, x, dtype, location, E_);
+    x_ = dst;
+  }
+
+  void upload_convert(T* dst, const void* src, int dtype, int location, int64_t n) {
+    const bool same = (dtype == 1) == (sizeof(T) == 4);
+    const cudaMemcpyKind kind = location == NTFG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (same) {
+      NTFG_CUDA(cudaMemcpyAsync(dst, src, size_t(n) * sizeof(T), kind, c_.stream));
+      return;
+    }
+    // convert in chunks through a device staging buffer
+    const int64_t chunk = int64_t(1) << 26;
+    const size_t esz = dtype == 1 ? 4 : 8;
+    void* tmp = c_.bufs.get("cp.xstage", size_t(std::min(n, chunk)) * esz);
+    for (int64_t b = 0; b < n; b += chunk) {
+      const int64_t len = std::min(chunk, n - b);
+      NTFG_CUDA(cudaMemcpyAsync(tmp, static_cast<const char*>(src) + b * esz, size_t(len) * esz, kind, c_.stream));
+      const int grid = int(std::min<int64_t>(ceil_div(len, 256), 4096));
+      if (dtype == 1)
+        convert_kernel<T, float><<<grid, 256, 0, c_.stream>>>(static_cast<const float*>(tmp), len, dst + b);
+      else
+        convert_kernel<T, double><<<grid, 256, 0, c_.stream>>>(static_cast<const double*>(tmp), len, dst + b);
+      NTFG_LAUNCHED(c_);
+    }
+  }
+
+  void set_factors_host(const double* f) {
+    c_.h2d(A_, f, factor_doubles() * sizeof(double));
+    stage(A(N_ - 1), stage_);
+  }
+  void get_factors_host(double* f) { c_.d2h(f, A_, factor_doubles() * sizeof(double)); }
+  void restage() { stage(A(N_ - 1), stage_); }
+
+  // ---- scratch for P / Q -----------------------------------------------------
+  void ensure_pq() {
+    if (!p_) p_ = c_.buf<T>("cp.p", size_t(E_));
+    if (!q_ && beta_ != 1.0) q_ = c_.buf<T>("cp.q", size_t(E_));
+  }
+  T* p() { ensure_pq(); return p_; }
+  T* q() { ensure_pq(); return q_; }
+  void set_pq_external(T* p, T* q) { p_ = p; q_ = q; }
+
+  // ---- loss bookkeeping ----------------------------------------------------------
+  void bind_losses(double* losses) { losses_ = losses; }
+  void reset_counter() { NTFG_CUDA(cudaMemsetAsync(counter_, 0, sizeof(int), c_.stream)); }
+  void reset_flags() { NTFG_CUDA(cudaMemsetAsync(flags_, 0, sizeof(unsigned), c_.stream)); }
+  unsigned* flags() const { return flags_; }
+
+  // ---- kernels -----------------------------------------------------------------------
+  void stage(const double* src, T* dst) {
+    const int64_t n = g_.K * RP_;
+    stage_kernel<T><<<int(ceil_div(n, 256)), 256, 0, c_.stream>>>(src, g_.K, int(R_), RP_, dst);
+    NTFG_LAUNCHED(c_);
+  }
+
+  int64_t recon_work() const {
+    const int KT = recon_kt();
+    return ceil_div(g_.rows, kRB) * ceil_div(g_.K, 256 * KT);
+  }
+  int recon_kt() const { return (sizeof(T) == 4 && RP_ <= 32) ? 2 : 1; }
+
+  // Xhat of the model `fac` (prefix modes) with staged last factor `alast`;
+  // writes P/Q (nullable) and/or the objective into losses[counter].
+  void recon(const double* const* fac, const T* alast, T* pout, T* qout, bool objective,
+             T* xhout = nullptr) {
+    ReconParams<T> p{};
+    p.g = g_;
+    p.R = int(R_);
+    for (int m = 0; m < N_; ++m) p.fac[m] = fac[m];
+    p.alast = alast;
+    p.x = x_;
+    p.pout = pout;
+    p.qout = qout;
+    p.xhout = xhout;
+    p.obj = objective ? objpart_ : nullptr;
+    p.flags = flags_;
+    p.beta = beta_;
+    p.eps = eps_;
+    p.bk = bk_;
+    const int KT = recon_kt();
+    p.ktiles = int(ceil_div(g_.K, 256 * KT));
+    p.work = recon_work();
+    const dim3 grid(recon_grid_), block(256);
+    switch (RP_) {
+      case 8: launch_recon<8>(p, grid, block); break;
+      case 16: launch_recon<16>(p, grid, block); break;
+      case 32: launch_recon<32>(p, grid, block); break;
+      default: launch_recon<64>(p, grid, block); break;
+    }
+    if (objective) finish_objective();
+  }
+
+  void finish_objective() {
+    const double inv = 1.0 / double(E_global_);
+    if (sharded_) {
+      objective_finalize_kernel<<<1, 256, 0, c_.stream>>>(objpart_, recon_grid_, inv, losses_, counter_, raw_);
+      NTFG_LAUNCHED(c_);
+      allreduce(raw_, 1);
+      objective_scale_kernel<<<1, 1, 0, c_.stream>>>(raw_, inv, losses_, counter_);
+      NTFG_LAUNCHED(c_);
+    } else {
+      objective_finalize_kernel<<<1, 256, 0, c_.stream>>>(objpart_, recon_grid_, inv, losses_, counter_, nullptr);
+      NTFG_LAUNCHED(c_);
+    }
+  }
+
+  // Mode-n contraction of one or two streams (reference cp_contract,
+  // tensor.cpp:372-406) into per-unit partials, then the fp64 second stage
+  // + MU step.  mfac[s][m] are the factors multiplied in for stream s.
+  struct Stream {
+    const T* src;
+    const double* fac[kMaxOrder];
+  };
+
+  struct Plan {
+    bool caseA;
+    int RC, KT, ktiles, grid;
+    int64_t In, units, S, An, Bn;
+  };
+
+  Plan plan(int n) const {
+    Plan pl{};
+    pl.caseA = (n == N_ - 1);
+    const int RCmax = sizeof(T) == 4 ? 64 : 32;
+    pl.RC = R_ <= 8 ? 8 : R_ <= 16 ? 16 : R_ <= 32 ? 32 : RCmax;
+    pl.KT = (sizeof(T) == 4 && pl.RC <= 32) ? 2 : 1;
+    pl.ktiles = int(ceil_div(g_.K, 128 * pl.KT));
+    pl.In = g_.dims[n];
+    pl.S = 1;
+    pl.An = 1;
+    pl.Bn = 1;
+    if (pl.caseA) {
+      pl.units = std::min<int64_t>(g_.rows, int64_t(2) * c_.sm_count);
+    } else {
+      for (int m = 0; m < n; ++m) pl.An *= g_.dims[m];
+      for (int m = n + 1; m < N_ - 1; ++m) pl.Bn *= g_.dims[m];
+      const int64_t tot = pl.An * pl.Bn;
+      pl.S = std::max<int64_t>(1, std::min<int64_t>(ceil_div(int64_t(4) * c_.sm_count, pl.In),
+                                                    std::max<int64_t>(1, tot / 16)));
+      pl.units = pl.In * pl.S;
+    }
+    pl.grid = int(std::min<int64_t>(pl.units, int64_t(2) * c_.sm_count));
+    return pl;
+  }
+
+  // Allocate every buffer a fit can touch (no cudaMalloc during graph capture).
+  void prealloc(int ns) {
+    size_t a = 0, b = 0;
+    for (int n = 0; n < N_; ++n) {
+      const Plan pl = plan(n);
+      if (pl.caseA) a = std::max(a, size_t(ns) * pl.units * g_.K * RP_);
+      else b = std::max(b, size_t(ns) * pl.In * pl.S * RP_);
+    }
+    partA_ = c_.buf<T>("cp.partA", std::max<size_t>(a, 1));
+    partB_ = c_.buf<double>("cp.partB", std::max<size_t>(b, 1));
+    ensure_pq();
+  }
+
+  // raw contraction of stream 0 into numden[0:In*R] (cp_contract API)
+  void contract_numden(int n, const Stream* st, double* scratch) {
+    contract_and_update(n, 1, st, true, scratch, scratch, nullptr, nullptr, nullptr, nullptr, 1);
+  }
+
+  void contract_and_update(int n, int ns, const Stream* st, bool den_closed,
+                           const double* anchor, double* out, const double* ref, double* c1,
+                           double* c2, T* stage_out, int force_phase = -1) {
+    if (!partA_) prealloc(2);
+    const Plan pl = plan(n);
+    const bool caseA = pl.caseA;
+    const int RC = pl.RC;
+    const int ktiles = pl.ktiles;
+    const int64_t In = pl.In, units = pl.units, S = pl.S, An = pl.An, Bn = pl.Bn;
+    const int grid = pl.grid;
+    T* partA = caseA ? partA_ : nullptr;
+    double* partB = caseA ? nullptr : partB_;
+
+    for (int r0 = 0; r0 < R_; r0 += RC) {
+      if (ns == 2) {
+        ContractParams<T, 2> p{};
+        fill_contract(p, n, r0, caseA, units, S, An, Bn, partA, partB, ktiles, st, 2);
+        launch_contract<2>(p, RC, grid);
+      } else {
+        ContractParams<T, 1> p{};
+        fill_contract(p, n, r0, caseA, units, S, An, Bn, partA, partB, ktiles, st, 1);
+        launch_contract<1>(p, RC, grid);
+      }
+    }
+
+    FinalizeParams<T> f{};
+    f.caseA = caseA;
+    f.In = In;
+    f.R = int(R_);
+    f.RP = RP_;
+    f.units = units;
+    f.S = S;
+    f.partA = partA;
+    f.partB = partB;
+    f.den_closed = den_closed;
+    f.colprod = colprod_;
+    f.numden = numden_;
+    f.anchor = anchor;
+    f.out = out;
+    f.ref = ref;
+    f.chi1 = c1;
+    f.chi2 = c2;
+    f.stage = stage_out;
+    f.gamma = gamma_;
+    f.eps = eps_;
+    f.beta = beta_;
+    f.flags = flags_;
+    const int fgrid = int(ceil_div(In * RP_, 256));
+    if (force_phase == 1) {
+      f.phase = 1;
+      finalize_kernel<T><<<fgrid, 256, 0, c_.stream>>>(f);
+      NTFG_LAUNCHED(c_);
+      return;
+    }
+    if (sharded_ && n != 0) {
+      // data-parallel: local partial sums -> allreduce -> identical MU on all ranks
+      f.phase = 1;
+      finalize_kernel<T><<<fgrid, 256, 0, c_.stream>>>(f);
+      NTFG_LAUNCHED(c_);
+      allreduce(numden_, size_t(2) * In * R_);
+      f.phase = 2;
+    } else {
+      f.phase = 0;
+    }
+    finalize_kernel<T><<<fgrid, 256, 0, c_.stream>>>(f);
+    NTFG_LAUNCHED(c_);
+  }
+
+  // beta = 1 closed-form denominator prod_{m != skip} colsum(F_m)
+  void colprod(const double* const* fac, int skip) {
+    ColsumParams p{};
+    p.order = N_;
+    p.skip = skip;
+    p.R = int(R_);
+    for (int m = 0; m < N_; ++m) {
+      p.rows[m] = g_.dims[m];
+      p.fac[m] = fac[m];
+    }
+    p.out = colsum_;
+    colsum_kernel<<<N_, 256, 0, c_.stream>>>(p);
+    NTFG_LAUNCHED(c_);
+    if (sharded_ && skip != 0) allreduce(colsum_, size_t(R_));  // slab-local mode-0 colsum
+    colprod_kernel<<<int(ceil_div(R_, 64)), 64, 0, c_.stream>>>(colsum_, N_, skip, int(R_), colprod_);
+    NTFG_LAUNCHED(c_);
+  }
+
+  // ---- solver steps ----------------------------------------------------------------------
+
+  // cp_block_update_anchored (cp.cpp:109-123); anchor == A(n) for the plain path.
+  void block_update(int n, const double* anchor, bool objective) {
+    const double* fac[kMaxOrder];
+    for (int m = 0; m < N_; ++m) fac[m] = (m == n) ? anchor : A(m);
+    const T* alast = stage_;
+    if (n == N_ - 1 && anchor != A(n)) {
+      stage(anchor, stage_anchor_);
+      alast = stage_anchor_;
+    }
+    ensure_pq();
+    recon(fac, alast, p_, beta_ != 1.0 ? q_ : nullptr, objective);
+    const bool closed = beta_ == 1.0;
+    if (closed) colprod(fac, n);
+    Stream st[2];
+    st[0].src = p_;
+    st[1].src = q_;
+    for (int m = 0; m < N_; ++m) st[0].fac[m] = st[1].fac[m] = fac[m];
+    contract_and_update(n, closed ? 1 : 2, st, closed, anchor, A(n), nullptr, nullptr, nullptr,
+                        n == N_ - 1 ? stage_ : nullptr);
+  }
+
+  // bcomm_sweep (cp.cpp:131-135), objective of the incoming model fused into block 0
+  void bcomm_sweep(bool fuse_objective) {
+    for (int n = 0; n < N_; ++n) block_update(n, A(n), fuse_objective && n == 0);
+  }
+
+  void bcomm_sweep_anchored(const double* anchors) {
+    for (int n = 0; n < N_; ++n) block_update(n, anchors + off_[n], false);
+  }
+
+  // make_jcomm_reference (cp.cpp:202-208): ref := A, chi := A (exact: chi(Z,Z) = Z)
+  void jcomm_reference(bool objective) {
+    const size_t bytes = factor_doubles() * sizeof(double);
+    c_.d2d(Aref_, A_, bytes);
+    c_.d2d(chi1_, A_, bytes);
+    c_.d2d(chi2_, A_, bytes);
+    const double* fac[kMaxOrder];
+    for (int m = 0; m < N_; ++m) fac[m] = A(m);
+    ensure_pq();
+    recon(fac, stage_, p_, beta_ != 1.0 ? q_ : nullptr, objective);
+  }
+
+  // jcomm_inner_update (cp.cpp:210-229)
+  void jcomm_inner(int n) {
+    const bool closed = beta_ == 1.0;
+    const double* c2[kMaxOrder];
+    for (int m = 0; m < N_; ++m) c2[m] = chi2_ + off_[m];
+    if (closed) colprod(c2, n);
+    Stream st[2];
+    st[0].src = p_;
+    st[1].src = q_;
+    for (int m = 0; m < N_; ++m) {
+      st[0].fac[m] = chi1_ + off_[m];
+      st[1].fac[m] = chi2_ + off_[m];
+    }
+    contract_and_update(n, closed ? 1 : 2, st, closed, Aref_ + off_[n], A(n), Aref_ + off_[n],
+                        chi1_ + off_[n], chi2_ + off_[n], n == N_ - 1 ? stage_ : nullptr);
+  }
+
+  // jcomm_outer_step (cp.cpp:231-240)
+  void jcomm_outer(int inner_steps, bool fuse_objective) {
+    jcomm_reference(fuse_objective);
+    for (int l = 0; l < inner_steps; ++l)
+      for (int n = 0; n < N_; ++n) jcomm_inner(n);
+  }
+
+  const T* x() const { return x_; }
+  unsigned* flag_ptr() const { return flags_; }
+  double* chi1_all() const { return chi1_; }
+  double* chi2_all() const { return chi2_; }
+  T* stage_last() const { return stage_; }
+  double* numden() const { return numden_; }
+
+  // standalone objective of the current model
+  void objective() {
+    const double* fac[kMaxOrder];
+    for (int m = 0; m < N_; ++m) fac[m] = A(m);
+    recon(fac, stage_, nullptr, nullptr, true);
+  }
+
+  double* Aref_all() const { return Aref_; }
+  double* anchors() const { return anch_; }
+  int64_t offset(int m) const { return off_[m]; }
+  bool sharded() const { return sharded_; }
+  int64_t max_dim() const {
+    int64_t d = 1;
+    for (int m = 0; m < N_; ++m) d = std::max(d, g_.dims[m]);
+    return d;
+  }
+
+  void allreduce(double* buf, size_t count) {
+    if (!c_.allreduce) return;
+    if (c_.allreduce(c_.allreduce_user, buf, count, c_.stream) != 0)
+      throw Error(NTFG_ERR_COMM, "allreduce hook failed");
+  }
+
+ private:
+  template <int RP>
+  void launch_recon(const ReconParams<T>& p, dim3 grid, dim3 block) {
+    constexpr int KT = (sizeof(T) == 4 && RP <= 32) ? 2 : 1;
+    recon_kernel<T, RP, KT><<<grid, block, 0, c_.stream>>>(p);
+    NTFG_LAUNCHED(c_);
+  }
+
+  template <int NS>
+  void fill_contract(ContractParams<T, NS>& p, int n, int r0, bool caseA, int64_t units, int64_t S,
+                     int64_t An, int64_t Bn, T* partA, double* partB, int ktiles, const Stream* st,
+                     int ns) {
+    p.g = g_;
+    p.n = n;
+    p.R = int(R_);
+    p.RP = RP_;
+    p.r0 = r0;
+    for (int s = 0; s < ns; ++s) {
+      p.src[s] = st[s].src;
+      for (int m = 0; m < N_; ++m) p.mfac[s][m] = st[s].fac[m];
+      p.lastfac[s] = st[s].fac[N_ - 1];
+    }
+    p.caseA = caseA;
+    p.units = units;
+    p.S = S;
+    p.An = An;
+    p.Bn = Bn;
+    p.partA = partA;
+    p.partB = partB;
+    p.ktiles = ktiles;
+  }
+
+  template <int NS>
+  void launch_contract(const ContractParams<T, NS>& p, int RC, int grid) {
+    const dim3 block(NS * 128);
+    if constexpr (sizeof(T) == 4) {
+      switch (RC) {
+        case 8: contract_kernel<T, 8, 2, NS><<<grid, block, 0, c_.stream>>>(p); break;
+        case 16: contract_kernel<T, 16, 2, NS><<<grid, block, 0, c_.stream>>>(p); break;
+        case 32: contract_kernel<T, 32, 2, NS><<<grid, block, 0, c_.stream>>>(p); break;
+        default: contract_kernel<T, 64, 1, NS><<<grid, block, 0, c_.stream>>>(p); break;
+      }
+    } else {
+      switch (RC) {
+        case 8: contract_kernel<T, 8, 1, NS><<<grid, block, 0, c_.stream>>>(p); break;
+        case 16: contract_kernel<T, 16, 1, NS><<<grid, block, 0, c_.stream>>>(p); break;
+        default: contract_kernel<T, 32, 1, NS><<<grid, block, 0, c_.stream>>>(p); break;
+      }
+    }
+    NTFG_LAUNCHED(c_);
+  }
+
+  Context& c_;
+  int N_;
+  int64_t R_;
+  int RP_;
+  double beta_, eps_, gamma_;
+  int bk_;
+  Geom g_{};
+  int64_t E_, E_global_;
+  bool sharded_ = false;
+  std::vector<int64_t> off_;
+  const T* x_ = nullptr;
+  T* p_ = nullptr;
+  T* q_ = nullptr;
+  double *A_, *Aref_, *chi1_, *chi2_, *anch_;
+  T *stage_, *stage_anchor_;
+  double *colsum_, *colprod_, *objpart_, *raw_, *numden_;
+  double* losses_ = nullptr;
+  T* partA_ = nullptr;
+  double* partB_ = nullptr;
+  unsigned* flags_;
+  int* counter_;
+  int recon_grid_;
+};
+
+}  // namespace ntfg
