@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Benchmark: J-CoMM outer iterations/s on BASELINE config C2.
+
+Workload (BASELINE.json configs[1]): dense 3-way CP, 512x512x512 fp32, R = 32,
+joint-MM with 5 inner sweeps per outer iteration; data = [[A,B,C]] (U[0,1)
+factors) times Gamma(10, 0.1) noise, init U[0.1, 1.1).  One "step" = one
+outer iteration (reference cache build + 15 inner block updates, objective
+fused).  The headline beta is 0.5; all four betas of the config are measured
+and reported under "per_beta".  Data is synthetic (seeded) and generated on
+the GPU; X, P~, Q~ (1.5 GB) exceed the 126 MB L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 runs under torchrun: X is split into mode-0 slabs, factors replicated,
+the Num/Den partials are allreduced (NCCL) -- strong scaling of the same job.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np
+
+DIMS = (512, 512, 512)
+RANK = 32
+INNER = 5
+BETAS = [0.5, 0.0, 1.0, 1.5]
+HEADLINE_BETA = 0.5
+METRIC = "MM outer iterations/sec (J-CoMM, C2 512^3 R=32 L=5)"
+FFMA_PEAK_T = 35.4  # measured FP32 FMA/s (T) on this pool's B200, profiles/r01_ubench.log
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# synthetic data
+
+def make_problem(dims, rank, seed, row0, row1, device):
+    """Truth U[0,1) factors, X = [[A,B,C]] * Gamma(10, 0.1) (fp32 on `device`),
+    init U[0.1, 1.1).  Rows [row0, row1) of mode 0 belong to this rank."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    truth = [torch.rand(d, rank, generator=g, dtype=torch.float64) for d in dims]
+    t0 = truth[0][row0:row1].to(device)
+    rest = [t.to(device) for t in truth[1:]]
+    x = torch.einsum("ir,jr,kr->ijk", t0, rest[0], rest[1])
+    gc = torch.Generator(device=device).manual_seed(seed + 7)
+    shape = (dims[0],) + tuple(dims[1:])
+    alpha = torch.full(shape, 10.0, device=device, dtype=torch.float32)
+    noise = torch._standard_gamma(alpha, generator=gc)[row0:row1] * 0.1
+    del alpha
+    x = (x * noise.double()).float().contiguous()
+    del noise
+    rng = np.random.default_rng(seed + 1)
+    init = [0.1 + rng.random((d, rank)) for d in dims]
+    init[0] = init[0][row0:row1].copy()
+    return x, init
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(args, rank_id, world, local_rank):
+    import torch
+    import paper_2602_14683_b200 as ntf
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    row0 = DIMS[0] * rank_id // world
+    row1 = DIMS[0] * (rank_id + 1) // world
+    x, init = make_problem(DIMS, RANK, 0, row0, row1, dev)
+    torch.cuda.synchronize()
+    ctx = ntf.Context(local_rank)
+    # a dedicated (capturable) stream shared by torch and the engine
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    shard = None
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        comm = torch.zeros(2 * max(DIMS) * RANK + 8, dtype=torch.float64, device=dev)
+        ctx.set_comm_buffer(comm.data_ptr(), comm.numel())
+
+        def allreduce(ptr, count, stream):
+            dist.all_reduce(comm[:count])
+
+        ctx.set_allreduce(allreduce)
+        shard = (DIMS[0], row0)
+
+    def fit(beta, iters, **kw):
+        cfg = ntf.FitConfig(beta=beta, rank=RANK, inner_steps=INNER, max_iters=iters, precision="f32", **kw)
+        return ntf.jcomm_fit(x, init, cfg, ctx=ctx, shard=shard)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    per_beta = {}
+    launches = None
+    sampler = ClockSampler(local_rank) if rank_id == 0 else None
+    if sampler:
+        sampler.start()
+    for beta in BETAS:
+        fit(beta, args.warmup)               # W untimed warm-up outer iterations
+        barrier()
+        res = fit(beta, args.steps)          # exactly K timed outer iterations
+        barrier()
+        st = ctx.stats()
+        ms = max_over_ranks(st["device_ms"])  # CUDA events around the K steps
+        per_beta[beta] = {"outer_it_per_s": args.steps / (ms * 1e-3), "ms_per_step": ms / args.steps,
+                          "final_loss": res.trace[-1].loss}
+        if beta == HEADLINE_BETA:
+            launches = st["kernel_launches"]
+    clocks = sampler.stop() if sampler else None
+
+    # per-kernel timing of the dominant kernel (eager launches, CUDA events on the launch stream)
+    ctx.set_profiling(True)
+    fit(HEADLINE_BETA, min(args.steps, 5))
+    pst = ctx.stats()
+    ctx.set_profiling(False)
+
+    # end to end through the public API with host (pinned) X: H2D + fit + D2H in the timed region
+    e2e = None
+    if args.e2e:
+        xh = x.cpu().pin_memory()
+        fit_h = lambda it: ntf.jcomm_fit(xh, init, ntf.FitConfig(beta=HEADLINE_BETA, rank=RANK, inner_steps=INNER,
+                                                              max_iters=it, precision="f32"), ctx=ctx, shard=shard)
+        fit_h(1)
+        barrier()
+        t0 = time.perf_counter()
+        fit_h(args.steps)
+        barrier()
+        el = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": args.steps / el, "unit": "outer_it/s",
+               "h2d_bytes_per_step": int(xh.numel() * 4 + sum(a.size * 8 for a in init)),
+               "d2h_bytes_per_step": int(sum(a.size * 8 for a in init) + (args.steps + 1) * 24),
+               "note": "one step = one public-API fit call of K outer iterations from pinned host X "
+                       "(X upload + factor/trace download inside the timed region); value = K / wall time"}
+        del xh
+
+    return per_beta, launches, pst, clocks, e2e
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (compiled unmodified reference; oracle/_ref) or the NumPy port
+
+def cpu_sample(steps_per_thread: int = 1, slab: int = 4, threads: int = 0, beta: float = HEADLINE_BETA):
+    """Times the reference solver on mode-0 slabs (slab x 512 x 512) of the C2
+    workload, one independent slab per host thread; returns C2-equivalent
+    outer it/s = entries processed per second / |X|."""
+    from oracle import ref as R
+    threads = threads or (os.cpu_count() or 1)
+    rng = np.random.default_rng(3)
+    dims = (slab,) + DIMS[1:]
+    truth = [rng.random((d, RANK)) for d in dims]
+    from oracle import ntf_oracle as O
+    x = O.cp_reconstruct(truth) * rng.gamma(10.0, 0.1, size=dims)
+    init = [0.1 + rng.random((d, RANK)) for d in dims]
+    kind = "reference" if R.available() else "port"
+    times = [0.0] * threads
+
+    def work(i):
+        if kind == "reference":
+            sec, _ = R.cp_time_outer("jcomm", x, init, beta, steps_per_thread, inner_steps=INNER)
+        else:
+            t0 = time.perf_counter()
+            f = [a.copy() for a in init]
+            for _ in range(steps_per_thread):
+                f = O.jcomm_outer_step(f, x, beta, INNER, 1e-12)
+            sec = time.perf_counter() - t0
+        times[i] = sec
+
+    t0 = time.perf_counter()
+    th = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    wall = time.perf_counter() - t0
+    entries = threads * steps_per_thread * int(np.prod(dims))
+    value = entries / wall / float(np.prod(DIMS))
+    return {"value": value, "unit": "outer_it/s", "cores": threads, "kind": kind,
+            "sample": f"{threads} threads x {steps_per_thread} J-CoMM outer step(s) (L={INNER}, beta={beta}) "
+                      f"on independent {slab}x512x512 fp64 slabs of the C2 workload; "
+                      f"C2-equivalent rate = entries/s / 512^3 (wall {wall:.2f} s)"}
+
+
+def run_reference(args, rank_id):
+    if rank_id != 0:
+        return
+    cpu_sample(1)  # warm the page cache / threads
+    vals = []
+    samples = None
+    for _ in range(args.warmup):
+        cpu_sample(1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s = cpu_sample(1)
+        vals.append(s["value"])
+        samples = s
+    el = time.perf_counter() - t0
+    value = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "outer_it/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2: CP 512^3 R=32 J-CoMM L=5 beta=0.5 (mode-0 slab samples)",
+                       "global_batch": 1, "seq_len": 0, "parallelism": "host threads"},
+            "cpu_baseline": {"value": value, "unit": "outer_it/s", "cores": samples["cores"],
+                             "kind": samples["kind"], "sample": samples["sample"]},
+            "e2e": {"value": value, "unit": "outer_it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": el}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank_id = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank_id)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    per_beta, launches, pst, clocks, e2e = run_ours(args, rank_id, world, local_rank)
+
+    if rank_id == 0:
+        E = int(np.prod(DIMS))
+        peak, peak_src = peaks()
+        # dominant kernel: K3 contraction pass (15 of the 16 streaming passes per outer)
+        avg_ms = pst["contract_ms"] / max(1, pst["contract_launches"])
+        ebytes = E * 2 * 4 // world  # P~ and Q~ fp32 read once per launch (beta != 1)
+        achieved = ebytes / (avg_ms * 1e-3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_contract_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        fma_rate = (E // world) * 2 * RANK / (avg_ms * 1e-3) / 1e12
+        head = per_beta[HEADLINE_BETA]
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_sample(1)
+            except Exception as ex:  # the baseline must never sink the bench line
+                cpu = {"value": None, "unit": "outer_it/s", "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+        line = {
+            "metric": METRIC, "value": head["outer_it_per_s"], "unit": "outer_it/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded GPU generator: U[0,1) CP truth x Gamma(10,0.1); init U[0.1,1.1))",
+            "config": {"workload": "C2: dense CP 512x512x512 fp32, R=32, J-CoMM L=5, beta=0.5 headline",
+                       "global_batch": 1, "seq_len": 0, "parallelism": f"mode-0 slabs dp{world}",
+                       "l2": "inputs (X 0.5 GB, P~/Q~ 1 GB) exceed L2; no flush"},
+            "per_beta": {str(b): v for b, v in per_beta.items()},
+            "roofline": {"bound": "hbm", "kernel": "contract_kernel (K3 J-CoMM inner pass)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "peak_source": peak_src, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": ebytes, "avg_launch_ms": avg_ms,
+                         "fma_rate_tflops_equiv": fma_rate, "fma_frac": fma_rate / FFMA_PEAK_T},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "kernel_breakdown_ms_per_step": {
+                "recon": pst["recon_ms"] / max(1, min(args.steps, 5)),
+                "contract": pst["contract_ms"] / max(1, min(args.steps, 5)),
+                "other": (pst["device_ms"] - pst["recon_ms"] - pst["contract_ms"]) / max(1, min(args.steps, 5))},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -92,8 +92,15 @@ typedef struct ntfg_shard {
 typedef struct ntfg_stats {
   uint64_t kernel_launches;   /* kernels enqueued by the last call (graph nodes counted per replay) */
   uint64_t graph_launches;
-  double device_ms;           /* device time of the last fit's timed steps */
-  double objective_ms;        /* device time of standalone objective passes */
+  double device_ms;           /* device time of the last fit's timed steps (CUDA events) */
+  /* per-kernel-class device time, filled only when profiling is enabled
+   * (eager launches bracketed by CUDA events on the context stream) */
+  double recon_ms;            /* K2/K5 reconstruction + weights (+objective) passes */
+  uint64_t recon_launches;
+  double contract_ms;         /* K3 contraction passes */
+  uint64_t contract_launches;
+  double other_ms;            /* finalize / small kernels */
+  uint64_t other_launches;
 } ntfg_stats;
 
 /* ---- context ------------------------------------------------------------- */
@@ -104,6 +111,11 @@ ntfg_status ntfg_context_destroy(ntfg_context* ctx);
 ntfg_status ntfg_context_set_stream(ntfg_context* ctx, void* cuda_stream);
 ntfg_status ntfg_context_set_allreduce(ntfg_context* ctx, ntfg_allreduce_fn fn, void* user);
 ntfg_status ntfg_context_stats(const ntfg_context* ctx, ntfg_stats* out);
+/* Per-kernel-class event timing for subsequent calls (disables graphs). */
+ntfg_status ntfg_context_set_profiling(ntfg_context* ctx, int enabled);
+/* Device buffer (>= capacity doubles) that allreduce payloads are staged
+ * through, so the hook always sees the same caller-owned buffer. */
+ntfg_status ntfg_context_set_comm_buffer(ntfg_context* ctx, double* device_buf, size_t capacity);
 /* Release cached device buffers. */
 ntfg_status ntfg_context_trim(ntfg_context* ctx);
 

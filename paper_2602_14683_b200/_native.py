@@ -56,7 +56,9 @@ class ShardC(C.Structure):
 
 class StatsC(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("graph_launches", C.c_uint64),
-                ("device_ms", C.c_double), ("objective_ms", C.c_double)]
+                ("device_ms", C.c_double), ("recon_ms", C.c_double), ("recon_launches", C.c_uint64),
+                ("contract_ms", C.c_double), ("contract_launches", C.c_uint64),
+                ("other_ms", C.c_double), ("other_launches", C.c_uint64)]
 
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
@@ -73,6 +75,8 @@ _SIGS = {
     "ntfg_context_set_allreduce": [_V, ALLREDUCE_FN, _V],
     "ntfg_context_stats": [_V, C.POINTER(StatsC)],
     "ntfg_context_trim": [_V],
+    "ntfg_context_set_profiling": [_V, C.c_int],
+    "ntfg_context_set_comm_buffer": [_V, _V, C.c_size_t],
     "ntfg_validate_fit_config": [C.POINTER(FitConfigC)],
     "ntfg_cp_fit": [_V, C.POINTER(FitConfigC), C.c_int32, C.c_uint32, _U, _V, C.c_int32, C.c_int32,
                     C.POINTER(ShardC), _P, C.POINTER(TraceRowC), _U],

@@ -213,8 +213,13 @@ class Context:
     def stats(self) -> dict:
         s = N.StatsC()
         _check(N.load().ntfg_context_stats(self.h, C.byref(s)))
-        return {"kernel_launches": s.kernel_launches, "graph_launches": s.graph_launches,
-                "device_ms": s.device_ms}
+        return {f: getattr(s, f) for f, _ in N.StatsC._fields_}
+
+    def set_profiling(self, enabled: bool):
+        _check(N.load().ntfg_context_set_profiling(self.h, int(bool(enabled))))
+
+    def set_comm_buffer(self, ptr: int, capacity: int):
+        _check(N.load().ntfg_context_set_comm_buffer(self.h, C.c_void_p(ptr), int(capacity)))
 
     def trim(self):
         _check(N.load().ntfg_context_trim(self.h))

@@ -145,6 +145,17 @@ NTFG_API ntfg_status ntfg_context_stats(const ntfg_context* ctx, ntfg_stats* out
   return NTFG_OK;
 }
 
+NTFG_API ntfg_status ntfg_context_set_profiling(ntfg_context* ctx, int enabled) {
+  return with_ctx(ctx, [&](ntfg::Context& c) { c.profile = enabled != 0; });
+}
+
+NTFG_API ntfg_status ntfg_context_set_comm_buffer(ntfg_context* ctx, double* buf, size_t cap) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    c.comm_buf = buf;
+    c.comm_cap = buf ? cap : 0;
+  });
+}
+
 NTFG_API ntfg_status ntfg_context_trim(ntfg_context* ctx) {
   return with_ctx(ctx, [&](ntfg::Context& c) {
     c.sync();

@@ -8,10 +8,13 @@
 // captured once into a CUDA graph by the fit driver.
 #pragma once
 #include <algorithm>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "cp_kernels.cuh"
 #include "engine.cuh"
+#include "stream_kernels.cuh"
 
 namespace ntfg {
 
@@ -42,6 +45,8 @@ class CpEngine {
       g_.rstride[m] = st;
       st *= g_.dims[m];
     }
+    g_.rstride[N_ - 1] = 1;
+    g_.init_fast();
     E_global_ = E_;
     if (shard) {
       if (shard->slab_begin + dims[0] > shard->global_dim0)
@@ -66,7 +71,12 @@ class CpEngine {
     raw_ = c_.buf<double>("cp.raw", 1);
     numden_ = c_.buf<double>("cp.numden", size_t(2) * max_dim() * R_);
     // objective partial count = recon grid
-    recon_grid_ = int(std::min<int64_t>(recon_work(), int64_t(c_.sm_count) * 4));
+    {
+      const int64_t kts = ceil_div(g_.K, int64_t(recon_tpb()) * recon_kt());
+      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(ceil_div(g_.rows, kRows),
+                                                                 ceil_div(int64_t(c_.sm_count) * 2, kts)));
+      recon_grid_ = int(kts * per);
+    }
     objpart_ = c_.buf<double>("cp.objpart", size_t(recon_grid_));
   }
 
@@ -126,6 +136,13 @@ class CpEngine {
     if (!q_ && beta_ != 1.0) q_ = c_.buf<T>("cp.q", size_t(E_));
   }
   T* p() { ensure_pq(); return p_; }
+  // Q buffer even at beta = 1 (the Tucker path contracts Q == 1 densely, as
+  // the reference does, tucker.cpp:52,72)
+  T* q_always() {
+    ensure_pq();
+    if (!q_) q_ = c_.buf<T>("cp.q", size_t(E_));
+    return q_;
+  }
   T* q() { ensure_pq(); return q_; }
   void set_pq_external(T* p, T* q) { p_ = p; q_ = q; }
 
@@ -143,15 +160,16 @@ class CpEngine {
   }
 
   int64_t recon_work() const {
-    const int KT = recon_kt();
-    return ceil_div(g_.rows, kRB) * ceil_div(g_.K, 256 * KT);
+    return ceil_div(g_.rows, kRows) * ceil_div(g_.K, int64_t(recon_tpb()) * recon_kt());
   }
-  int recon_kt() const { return (sizeof(T) == 4 && RP_ <= 32) ? 2 : 1; }
+  // two columns per thread (packed loads, FFMA2) when the row length allows
+  int recon_kt() const { return (sizeof(T) == 4 && RP_ <= 32 && g_.K % 2 == 0) ? 2 : 1; }
+  int recon_tpb() const { return g_.K > 128 * recon_kt() ? 256 : 128; }
 
   // Xhat of the model `fac` (prefix modes) with staged last factor `alast`;
   // writes P/Q (nullable) and/or the objective into losses[counter].
   void recon(const double* const* fac, const T* alast, T* pout, T* qout, bool objective,
-             T* xhout = nullptr) {
+             T* xhout = nullptr, const double* htab = nullptr) {
     ReconParams<T> p{};
     p.g = g_;
     p.R = int(R_);
@@ -161,21 +179,23 @@ class CpEngine {
     p.pout = pout;
     p.qout = qout;
     p.xhout = xhout;
+    p.htab = htab;
     p.obj = objective ? objpart_ : nullptr;
     p.flags = flags_;
     p.beta = beta_;
     p.eps = eps_;
     p.bk = bk_;
     const int KT = recon_kt();
-    p.ktiles = int(ceil_div(g_.K, 256 * KT));
+    p.ktiles = int(ceil_div(g_.K, int64_t(recon_tpb()) * KT));
     p.work = recon_work();
-    const dim3 grid(recon_grid_), block(256);
+    const int ph = c_.prof_begin(0);
     switch (RP_) {
-      case 8: launch_recon<8>(p, grid, block); break;
-      case 16: launch_recon<16>(p, grid, block); break;
-      case 32: launch_recon<32>(p, grid, block); break;
-      default: launch_recon<64>(p, grid, block); break;
+      case 8: launch_recon<8>(p); break;
+      case 16: launch_recon<16>(p); break;
+      case 32: launch_recon<32>(p); break;
+      default: launch_recon<64>(p); break;
     }
+    c_.prof_end(ph);
     if (objective) finish_objective();
   }
 
@@ -199,11 +219,12 @@ class CpEngine {
   struct Stream {
     const T* src;
     const double* fac[kMaxOrder];
+    const double* mtab = nullptr;  // case A row table (Tucker partial reconstruction)
   };
 
   struct Plan {
     bool caseA;
-    int RC, KT, ktiles, grid;
+    int RC, KT, TPS, ktiles, grid;
     int64_t In, units, S, An, Bn;
   };
 
@@ -212,14 +233,15 @@ class CpEngine {
     pl.caseA = (n == N_ - 1);
     const int RCmax = sizeof(T) == 4 ? 64 : 32;
     pl.RC = R_ <= 8 ? 8 : R_ <= 16 ? 16 : R_ <= 32 ? 32 : RCmax;
-    pl.KT = (sizeof(T) == 4 && pl.RC <= 32) ? 2 : 1;
-    pl.ktiles = int(ceil_div(g_.K, 128 * pl.KT));
+    pl.KT = (sizeof(T) == 4 && pl.RC <= 32 && g_.K % 2 == 0) ? 2 : 1;
+    pl.TPS = g_.K > 128 * pl.KT ? 256 : 128;
+    pl.ktiles = int(ceil_div(g_.K, int64_t(pl.TPS) * pl.KT));
     pl.In = g_.dims[n];
     pl.S = 1;
     pl.An = 1;
     pl.Bn = 1;
     if (pl.caseA) {
-      pl.units = std::min<int64_t>(g_.rows, int64_t(2) * c_.sm_count);
+      pl.units = std::min<int64_t>(g_.rows, int64_t(c_.sm_count) * (pl.TPS == 256 ? 1 : 2));
     } else {
       for (int m = 0; m < n; ++m) pl.An *= g_.dims[m];
       for (int m = n + 1; m < N_ - 1; ++m) pl.Bn *= g_.dims[m];
@@ -228,7 +250,8 @@ class CpEngine {
                                                     std::max<int64_t>(1, tot / 16)));
       pl.units = pl.In * pl.S;
     }
-    pl.grid = int(std::min<int64_t>(pl.units, int64_t(2) * c_.sm_count));
+    const int ns_max = beta_ == 1.0 ? 1 : 2;  // one CTA per SM at 512 threads
+    pl.grid = int(std::min<int64_t>(pl.units, int64_t(c_.sm_count) * (pl.TPS * ns_max >= 512 ? 1 : 2)));
     return pl;
   }
 
@@ -242,6 +265,7 @@ class CpEngine {
     }
     partA_ = c_.buf<T>("cp.partA", std::max<size_t>(a, 1));
     partB_ = c_.buf<double>("cp.partB", std::max<size_t>(b, 1));
+    partAd_ = c_.buf<double>("cp.partAd", std::max<size_t>(a / 8 + size_t(ns) * g_.K * RP_, 1));
     ensure_pq();
   }
 
@@ -263,24 +287,36 @@ class CpEngine {
     T* partA = caseA ? partA_ : nullptr;
     double* partB = caseA ? nullptr : partB_;
 
+    const int ph = c_.prof_begin(1);
     for (int r0 = 0; r0 < R_; r0 += RC) {
       if (ns == 2) {
         ContractParams<T, 2> p{};
         fill_contract(p, n, r0, caseA, units, S, An, Bn, partA, partB, ktiles, st, 2);
-        launch_contract<2>(p, RC, grid);
+        launch_contract<2>(p, pl, grid);
       } else {
         ContractParams<T, 1> p{};
         fill_contract(p, n, r0, caseA, units, S, An, Bn, partA, partB, ktiles, st, 1);
-        launch_contract<1>(p, RC, grid);
+        launch_contract<1>(p, pl, grid);
       }
     }
+    c_.prof_end(ph);
 
     FinalizeParams<T> f{};
+    if (caseA && units > 16) {
+      const int64_t per = 8, chunks = ceil_div(units, per), slice = In * RP_;
+      const int64_t total = int64_t(ns) * chunks * slice;
+      const int rgrid = int(std::min<int64_t>(ceil_div(total, 256), int64_t(c_.sm_count) * 8));
+      reduce_units_kernel<T><<<rgrid, 256, 0, c_.stream>>>(partA, units, per, chunks, slice, ns, partAd_);
+      NTFG_LAUNCHED(c_);
+      f.partAd = partAd_;
+      f.units = chunks;
+    } else {
+      f.units = units;
+    }
     f.caseA = caseA;
     f.In = In;
     f.R = int(R_);
     f.RP = RP_;
-    f.units = units;
     f.S = S;
     f.partA = partA;
     f.partB = partB;
@@ -430,16 +466,47 @@ class CpEngine {
 
   void allreduce(double* buf, size_t count) {
     if (!c_.allreduce) return;
-    if (c_.allreduce(c_.allreduce_user, buf, count, c_.stream) != 0)
+    double* target = buf;
+    if (c_.comm_buf) {
+      if (count > c_.comm_cap) throw Error(NTFG_ERR_COMM, "comm buffer too small");
+      c_.d2d(c_.comm_buf, buf, count * sizeof(double));
+      target = c_.comm_buf;
+    }
+    if (c_.allreduce(c_.allreduce_user, target, count, c_.stream) != 0)
       throw Error(NTFG_ERR_COMM, "allreduce hook failed");
+    if (target != buf) c_.d2d(buf, target, count * sizeof(double));
   }
 
  private:
-  template <int RP>
-  void launch_recon(const ReconParams<T>& p, dim3 grid, dim3 block) {
-    constexpr int KT = (sizeof(T) == 4 && RP <= 32) ? 2 : 1;
-    recon_kernel<T, RP, KT><<<grid, block, 0, c_.stream>>>(p);
+  template <typename K2, typename P>
+  void launch_dyn(K2 kern, dim3 grid, dim3 block, size_t smem, const P& p) {
+    // one attribute call per kernel (keyed by its address: many kernels share
+    // a signature, so a per-signature static would miss all but the first)
+    static std::mutex mu;
+    static std::set<const void*> done;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (done.insert(reinterpret_cast<const void*>(kern)).second)
+        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+                   "cudaFuncSetAttribute");
+    }
+    kern<<<grid, block, smem, c_.stream>>>(p);
     NTFG_LAUNCHED(c_);
+  }
+
+  template <int RP>
+  void launch_recon(const ReconParams<T>& p) {
+    constexpr int KT2 = (sizeof(T) == 4 && RP <= 32) ? 2 : 1;
+    const dim3 grid(recon_grid_);
+    if (recon_kt() == 2) {
+      if constexpr (KT2 == 2) {
+        if (recon_tpb() == 256) launch_dyn(recon2_kernel<T, RP, 2, 256>, grid, dim3(256), recon2_smem<T, 2, 256>(), p);
+        else launch_dyn(recon2_kernel<T, RP, 2, 128>, grid, dim3(128), recon2_smem<T, 2, 128>(), p);
+        return;
+      }
+    }
+    if (recon_tpb() == 256) launch_dyn(recon2_kernel<T, RP, 1, 256>, grid, dim3(256), recon2_smem<T, 1, 256>(), p);
+    else launch_dyn(recon2_kernel<T, RP, 1, 128>, grid, dim3(128), recon2_smem<T, 1, 128>(), p);
   }
 
   template <int NS>
@@ -455,35 +522,54 @@ class CpEngine {
       p.src[s] = st[s].src;
       for (int m = 0; m < N_; ++m) p.mfac[s][m] = st[s].fac[m];
       p.lastfac[s] = st[s].fac[N_ - 1];
+      p.mtab[s] = st[s].mtab;
     }
     p.caseA = caseA;
     p.units = units;
     p.S = S;
     p.An = An;
     p.Bn = Bn;
+    p.fB.init(Bn);
     p.partA = partA;
     p.partB = partB;
     p.ktiles = ktiles;
   }
 
+  template <int NS, int RC, int KT, int TPS>
+  void launch_c2(const ContractParams<T, NS>& p, int grid) {
+    launch_dyn(contract2_kernel<T, RC, KT, NS, TPS>, dim3(grid), dim3(NS * TPS),
+               contract2_smem<T, RC, KT, NS, TPS>(), p);
+  }
+  template <int NS, int RC, int KT>
+  void launch_c2t(const ContractParams<T, NS>& p, const Plan& pl, int grid) {
+    if (pl.TPS == 256) launch_c2<NS, RC, KT, 256>(p, grid);
+    else launch_c2<NS, RC, KT, 128>(p, grid);
+  }
+
   template <int NS>
-  void launch_contract(const ContractParams<T, NS>& p, int RC, int grid) {
-    const dim3 block(NS * 128);
+  void launch_contract(const ContractParams<T, NS>& p, const Plan& pl, int grid) {
     if constexpr (sizeof(T) == 4) {
-      switch (RC) {
-        case 8: contract_kernel<T, 8, 2, NS><<<grid, block, 0, c_.stream>>>(p); break;
-        case 16: contract_kernel<T, 16, 2, NS><<<grid, block, 0, c_.stream>>>(p); break;
-        case 32: contract_kernel<T, 32, 2, NS><<<grid, block, 0, c_.stream>>>(p); break;
-        default: contract_kernel<T, 64, 1, NS><<<grid, block, 0, c_.stream>>>(p); break;
+      if (pl.KT == 2) {
+        switch (pl.RC) {
+          case 8: launch_c2t<NS, 8, 2>(p, pl, grid); break;
+          case 16: launch_c2t<NS, 16, 2>(p, pl, grid); break;
+          default: launch_c2t<NS, 32, 2>(p, pl, grid); break;
+        }
+      } else {
+        switch (pl.RC) {
+          case 8: launch_c2t<NS, 8, 1>(p, pl, grid); break;
+          case 16: launch_c2t<NS, 16, 1>(p, pl, grid); break;
+          case 32: launch_c2t<NS, 32, 1>(p, pl, grid); break;
+          default: launch_c2t<NS, 64, 1>(p, pl, grid); break;
+        }
       }
     } else {
-      switch (RC) {
-        case 8: contract_kernel<T, 8, 1, NS><<<grid, block, 0, c_.stream>>>(p); break;
-        case 16: contract_kernel<T, 16, 1, NS><<<grid, block, 0, c_.stream>>>(p); break;
-        default: contract_kernel<T, 32, 1, NS><<<grid, block, 0, c_.stream>>>(p); break;
+      switch (pl.RC) {
+        case 8: launch_c2t<NS, 8, 1>(p, pl, grid); break;
+        case 16: launch_c2t<NS, 16, 1>(p, pl, grid); break;
+        default: launch_c2t<NS, 32, 1>(p, pl, grid); break;
       }
     }
-    NTFG_LAUNCHED(c_);
   }
 
   Context& c_;
@@ -505,6 +591,7 @@ class CpEngine {
   double* losses_ = nullptr;
   T* partA_ = nullptr;
   double* partB_ = nullptr;
+  double* partAd_ = nullptr;
   unsigned* flags_;
   int* counter_;
   int recon_grid_;

@@ -81,9 +81,51 @@ struct Context {
   ntfg_allreduce_fn allreduce = nullptr;
   void* allreduce_user = nullptr;
   ntfg_stats stats{};
+  bool profile = false;
+  double* comm_buf = nullptr;
+  size_t comm_cap = 0;
   BufferCache bufs;
   PinnedCache pinned;
   int sm_count = 148;
+
+  // ---- per-kernel-class profiling (eager mode) ----
+  struct ProfEv { int cls; cudaEvent_t a, b; };
+  std::vector<ProfEv> prof_events;
+  size_t prof_used = 0;
+  int prof_begin(int cls) {
+    if (!profile) return -1;
+    if (prof_used == prof_events.size()) {
+      ProfEv p{cls, nullptr, nullptr};
+      cuda_check(cudaEventCreate(&p.a), "cudaEventCreate");
+      cuda_check(cudaEventCreate(&p.b), "cudaEventCreate");
+      prof_events.push_back(p);
+    }
+    ProfEv& p = prof_events[prof_used];
+    p.cls = cls;
+    cuda_check(cudaEventRecord(p.a, stream), "cudaEventRecord");
+    return int(prof_used++);
+  }
+  void prof_end(int h) {
+    if (h < 0) return;
+    cuda_check(cudaEventRecord(prof_events[size_t(h)].b, stream), "cudaEventRecord");
+  }
+  void prof_collect() {
+    if (!profile) return;
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+    for (size_t i = 0; i < prof_used; ++i) {
+      float ms = 0.f;
+      cuda_check(cudaEventElapsedTime(&ms, prof_events[i].a, prof_events[i].b), "elapsed");
+      switch (prof_events[i].cls) {
+        case 0: stats.recon_ms += ms; stats.recon_launches++; break;
+        case 1: stats.contract_ms += ms; stats.contract_launches++; break;
+        default: stats.other_ms += ms; stats.other_launches++; break;
+      }
+    }
+    prof_used = 0;
+  }
+  ~Context() {
+    for (auto& p : prof_events) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+  }
 
   void activate() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
   template <typename T>

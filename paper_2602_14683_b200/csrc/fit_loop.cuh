@@ -36,7 +36,7 @@ inline std::vector<ntfg_trace_row> run_fit_loop(Context& c, const ntfg_fit_confi
                                                 unsigned* flags_dev) {
   const uint64_t K = cfg.max_iters;
   const bool check_each = cfg.tol > 0.0;
-  const bool graphs = cfg.use_graphs && c.allreduce == nullptr;
+  const bool graphs = cfg.use_graphs && c.allreduce == nullptr && !c.profile;
   std::vector<ntfg_trace_row> trace;
   double* hl = static_cast<double*>(c.pinned.get((K + 2) * sizeof(double)));
 
@@ -139,6 +139,7 @@ inline std::vector<ntfg_trace_row> run_fit_loop(Context& c, const ntfg_fit_confi
     float total = 0.f;
     NTFG_CUDA(cudaEventElapsedTime(&total, ev[0], ev[done]));
     c.stats.device_ms = total;
+    c.prof_collect();
   } catch (...) {
     cleanup();
     throw;

@@ -20,7 +20,7 @@
 namespace ntfg {
 
 // out[o][a][q] = sum_b in[o][b][q] * F(a, b), F(a,b) = trans ? M[b*na + a] : M[a*nb + b]
-__global__ void ttm_kernel(const double* __restrict__ in, int64_t outer, int64_t nb, int64_t inner,
+static __global__ void ttm_kernel(const double* __restrict__ in, int64_t outer, int64_t nb, int64_t inner,
                            const double* __restrict__ M, int64_t na, int trans,
                            double* __restrict__ out) {
   const int64_t total = outer * na * inner;
@@ -44,7 +44,7 @@ __global__ void ttm_kernel(const double* __restrict__ in, int64_t outer, int64_t
 // T(row, j) = sum_k S(row, k) F(k, j); F staged as T [K][JP] (zero padded).
 // One warp per row, lanes stride k; fp64 result.
 template <typename T, int JP>
-__global__ void __launch_bounds__(256) rowgemm_kernel(const T* __restrict__ S, int64_t rows,
+static __global__ void __launch_bounds__(256) rowgemm_kernel(const T* __restrict__ S, int64_t rows,
                                                       int64_t K, const T* __restrict__ F, int J,
                                                       double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
@@ -81,7 +81,7 @@ struct PairParams {
   double* out;  // [In][J_n]
 };
 
-__global__ void core_pair_kernel(const PairParams p) {
+static __global__ void core_pair_kernel(const PairParams p) {
   const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const int64_t Jn = p.J[p.n];
   if (idx >= p.In * Jn) return;
@@ -116,8 +116,21 @@ __global__ void core_pair_kernel(const PairParams p) {
   p.out[idx] = acc;
 }
 
+// out[o][q][m] = in[o][m][q]  (moves one axis to the back)
+static __global__ void moveaxis_last_kernel(const double* in, int64_t outer, int64_t mid, int64_t inner,
+                                     double* out) {
+  const int64_t total = outer * mid * inner;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t m = idx % mid;
+    const int64_t q = (idx / mid) % inner;
+    const int64_t o = idx / (mid * inner);
+    out[idx] = in[(o * mid + m) * inner + q];
+  }
+}
+
 // out = max(anchor (num / max(den, eps))^gamma, eps) elementwise, + chi.
-__global__ void mu_dense_kernel(const double* anchor, const double* num, const double* den,
+static __global__ void mu_dense_kernel(const double* anchor, const double* num, const double* den,
                                 int64_t n, double gamma, double eps, double beta, double* out,
                                 const double* ref, double* c1, double* c2, unsigned* flags) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
