@@ -226,7 +226,7 @@ def run_ours(args, rank_id, world, local_rank):
 # ---------------------------------------------------------------------------
 # CPU reference (compiled unmodified reference; oracle/_ref) or the NumPy port
 
-def cpu_sample(steps_per_thread: int = 1, slab: int = 4, threads: int = 0, beta: float = HEADLINE_BETA):
+def cpu_sample(steps_per_thread: int = 2, slab: int = 4, threads: int = 0, beta: float = HEADLINE_BETA):
     """Times the reference solver on mode-0 slabs (slab x 512 x 512) of the C2
     workload, one independent slab per host thread; returns C2-equivalent
     outer it/s = entries processed per second / |X|."""

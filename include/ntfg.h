@@ -210,7 +210,9 @@ ntfg_status ntfg_tucker_objective(ntfg_context* ctx, int32_t precision, double b
  *  0 block_core_update, 1 block_factor_update(mode), 2 tucker_bcomm_sweep,
  *  3 jcomm_tucker_outer_step(inner_steps),
  *  4 jcomm_inner_core_update and 5 jcomm_inner_factor_update(mode) against the
- *    reference model (ref_core, ref_factors) whose P~/Q~ are built from x. */
+ *    reference model (ref_core, ref_factors) whose P~/Q~ are built from x,
+ *  6 block_core_update_anchored (anchor core in ref_core),
+ *  7 block_factor_update_anchored(mode) (anchor I_mode x J_mode block in ref_factors). */
 ntfg_status ntfg_tucker_step(ntfg_context* ctx, int32_t precision, int32_t kind, double beta,
                              double eps, uint64_t inner_steps, uint32_t order,
                              const uint64_t* dims, const double* x, const uint64_t* ranks,

@@ -14,7 +14,7 @@
 
 #include "cp_kernels.cuh"
 #include "engine.cuh"
-#include "stream_kernels.cuh"
+#include "stream3_kernels.cuh"
 
 namespace ntfg {
 
@@ -70,14 +70,8 @@ class CpEngine {
     counter_ = c_.buf<int>("cp.counter", 1);
     raw_ = c_.buf<double>("cp.raw", 1);
     numden_ = c_.buf<double>("cp.numden", size_t(2) * max_dim() * R_);
-    // objective partial count = recon grid
-    {
-      const int64_t kts = ceil_div(g_.K, int64_t(recon_tpb()) * recon_kt());
-      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(ceil_div(g_.rows, kRows),
-                                                                 ceil_div(int64_t(c_.sm_count) * 2, kts)));
-      recon_grid_ = int(kts * per);
-    }
-    objpart_ = c_.buf<double>("cp.objpart", size_t(recon_grid_));
+    // objective partials: one per recon CTA (grid depends on the kernel variant)
+    objpart_ = c_.buf<double>("cp.objpart", size_t(std::max(recon_grid(false), recon_grid(true))));
   }
 
   int order() const { return N_; }
@@ -162,9 +156,24 @@ class CpEngine {
   int64_t recon_work() const {
     return ceil_div(g_.rows, kRows) * ceil_div(g_.K, int64_t(recon_tpb()) * recon_kt());
   }
-  // two columns per thread (packed loads, FFMA2) when the row length allows
+  // v2: two columns per thread (packed loads, FFMA2) when the row length allows
   int recon_kt() const { return (sizeof(T) == 4 && RP_ <= 32 && g_.K % 2 == 0) ? 2 : 1; }
   int recon_tpb() const { return g_.K > 128 * recon_kt() ? 256 : 128; }
+  // v3 (bulk-copy staging): rows must be 16-byte multiples
+  bool rows_tma_ok(const void* base) const {
+    return (g_.K * int64_t(sizeof(T))) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0;
+  }
+  int recon_kt3() const {
+    if (sizeof(T) == 4) return RP_ <= 16 ? 4 : RP_ <= 32 ? 2 : 1;
+    return RP_ <= 16 ? 2 : 1;
+  }
+  int recon_grid(bool v3) const {
+    const int64_t w = v3 ? int64_t(128) * recon_kt3() : int64_t(recon_tpb()) * recon_kt();
+    const int64_t kts = ceil_div(g_.K, w);
+    const int64_t per = std::max<int64_t>(1, std::min<int64_t>(ceil_div(g_.rows, kRows),
+                                                               ceil_div(int64_t(c_.sm_count) * (v3 ? 3 : 2), kts)));
+    return int(kts * per);
+  }
 
   // Xhat of the model `fac` (prefix modes) with staged last factor `alast`;
   // writes P/Q (nullable) and/or the objective into losses[counter].
@@ -185,8 +194,10 @@ class CpEngine {
     p.beta = beta_;
     p.eps = eps_;
     p.bk = bk_;
-    const int KT = recon_kt();
-    p.ktiles = int(ceil_div(g_.K, int64_t(recon_tpb()) * KT));
+    const bool v3 = rows_tma_ok(x_) && (!pout || rows_tma_ok(pout)) && (!qout || rows_tma_ok(qout));
+    recon_grid_ = recon_grid(v3);
+    recon_v3_ = v3;
+    p.ktiles = int(ceil_div(g_.K, v3 ? int64_t(128) * recon_kt3() : int64_t(recon_tpb()) * recon_kt()));
     p.work = recon_work();
     const int ph = c_.prof_begin(0);
     switch (RP_) {
@@ -223,25 +234,31 @@ class CpEngine {
   };
 
   struct Plan {
-    bool caseA;
+    bool caseA, v3;
     int RC, KT, TPS, ktiles, grid;
     int64_t In, units, S, An, Bn;
   };
 
-  Plan plan(int n) const {
+  Plan plan(int n, bool v3 = false) const {
     Plan pl{};
     pl.caseA = (n == N_ - 1);
+    pl.v3 = v3;
     const int RCmax = sizeof(T) == 4 ? 64 : 32;
     pl.RC = R_ <= 8 ? 8 : R_ <= 16 ? 16 : R_ <= 32 ? 32 : RCmax;
-    pl.KT = (sizeof(T) == 4 && pl.RC <= 32 && g_.K % 2 == 0) ? 2 : 1;
-    pl.TPS = g_.K > 128 * pl.KT ? 256 : 128;
+    if (v3) {
+      pl.KT = sizeof(T) == 4 ? (pl.RC <= 32 ? 4 : 1) : 2;
+      pl.TPS = 128;
+    } else {
+      pl.KT = (sizeof(T) == 4 && pl.RC <= 32 && g_.K % 2 == 0) ? 2 : 1;
+      pl.TPS = g_.K > 128 * pl.KT ? 256 : 128;
+    }
     pl.ktiles = int(ceil_div(g_.K, int64_t(pl.TPS) * pl.KT));
     pl.In = g_.dims[n];
     pl.S = 1;
     pl.An = 1;
     pl.Bn = 1;
     if (pl.caseA) {
-      pl.units = std::min<int64_t>(g_.rows, int64_t(c_.sm_count) * (pl.TPS == 256 ? 1 : 2));
+      pl.units = std::min<int64_t>(g_.rows, int64_t(c_.sm_count) * ((pl.TPS == 256 || v3) ? 1 : 2));
     } else {
       for (int m = 0; m < n; ++m) pl.An *= g_.dims[m];
       for (int m = n + 1; m < N_ - 1; ++m) pl.Bn *= g_.dims[m];
@@ -251,7 +268,8 @@ class CpEngine {
       pl.units = pl.In * pl.S;
     }
     const int ns_max = beta_ == 1.0 ? 1 : 2;  // one CTA per SM at 512 threads
-    pl.grid = int(std::min<int64_t>(pl.units, int64_t(c_.sm_count) * (pl.TPS * ns_max >= 512 ? 1 : 2)));
+    const int per_sm = v3 ? 1 : (pl.TPS * ns_max >= 512 ? 1 : 2);
+    pl.grid = int(std::min<int64_t>(pl.units, int64_t(c_.sm_count) * per_sm));
     return pl;
   }
 
@@ -259,13 +277,16 @@ class CpEngine {
   void prealloc(int ns) {
     size_t a = 0, b = 0;
     for (int n = 0; n < N_; ++n) {
-      const Plan pl = plan(n);
-      if (pl.caseA) a = std::max(a, size_t(ns) * pl.units * g_.K * RP_);
-      else b = std::max(b, size_t(ns) * pl.In * pl.S * RP_);
+      for (int v = 0; v < 2; ++v) {
+        const Plan pl = plan(n, v == 1);
+        if (pl.caseA) a = std::max(a, size_t(ns) * pl.units * g_.K * RP_);
+        else b = std::max(b, size_t(ns) * pl.In * pl.S * RP_);
+      }
     }
     partA_ = c_.buf<T>("cp.partA", std::max<size_t>(a, 1));
     partB_ = c_.buf<double>("cp.partB", std::max<size_t>(b, 1));
     partAd_ = c_.buf<double>("cp.partAd", std::max<size_t>(a / 8 + size_t(ns) * g_.K * RP_, 1));
+    if (beta_ == 1.0) n1num_ = c_.buf<double>("cp.n1num", factor_doubles() + size_t(max_dim()) * R_);
     ensure_pq();
   }
 
@@ -278,7 +299,9 @@ class CpEngine {
                            const double* anchor, double* out, const double* ref, double* c1,
                            double* c2, T* stage_out, int force_phase = -1) {
     if (!partA_) prealloc(2);
-    const Plan pl = plan(n);
+    bool v3 = true;
+    for (int s2 = 0; s2 < ns; ++s2) v3 = v3 && rows_tma_ok(st[s2].src);
+    const Plan pl = plan(n, v3);
     const bool caseA = pl.caseA;
     const int RC = pl.RC;
     const int ktiles = pl.ktiles;
@@ -433,12 +456,63 @@ class CpEngine {
                         chi1_ + off_[n], chi2_ + off_[n], n == N_ - 1 ? stage_ : nullptr);
   }
 
+  // beta = 1 (SURVEY.md 8(a) note N1): chi1(Z, Zref) == Zref exactly
+  // (fast_pow(x, 0) == 1, kernels.hpp:13), so every inner numerator
+  // cp_contract(P~, chi1(...)) depends only on P~ and the reference factors:
+  // it is computed once per outer iteration (one P~ pass per mode) and reused
+  // by all L sweeps; the denominator is the closed form of cp.cpp:224-225.
+  void n1_numerators() {
+    if (!n1num_) n1num_ = c_.buf<double>("cp.n1num", factor_doubles() + size_t(max_dim()) * R_);
+    Stream st[2];
+    st[0].src = p_;
+    st[1].src = p_;
+    for (int m = 0; m < N_; ++m) st[0].fac[m] = st[1].fac[m] = Aref_ + off_[m];
+    for (int n = 0; n < N_; ++n) {
+      contract_and_update(n, 1, st, true, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 1);
+      if (sharded_ && n != 0) allreduce(numden_, size_t(g_.dims[n]) * R_);
+      c_.d2d(n1num_ + off_[n], numden_, size_t(g_.dims[n]) * R_ * sizeof(double));
+    }
+  }
+
+  void jcomm_inner_n1(int n) {
+    const double* c2[kMaxOrder];
+    for (int m = 0; m < N_; ++m) c2[m] = chi2_ + off_[m];
+    colprod(c2, n);
+    FinalizeParams<T> f{};
+    f.In = g_.dims[n];
+    f.R = int(R_);
+    f.RP = RP_;
+    f.den_closed = 1;
+    f.colprod = colprod_;
+    f.phase = 2;
+    f.numden = n1num_ + off_[n];
+    f.anchor = Aref_ + off_[n];
+    f.out = A(n);
+    f.ref = Aref_ + off_[n];
+    f.chi1 = chi1_ + off_[n];
+    f.chi2 = chi2_ + off_[n];
+    f.stage = n == N_ - 1 ? stage_ : nullptr;
+    f.gamma = gamma_;
+    f.eps = eps_;
+    f.beta = beta_;
+    f.flags = flags_;
+    finalize_kernel<T><<<int(ceil_div(g_.dims[n] * RP_, 256)), 256, 0, c_.stream>>>(f);
+    NTFG_LAUNCHED(c_);
+  }
+
   // jcomm_outer_step (cp.cpp:231-240)
   void jcomm_outer(int inner_steps, bool fuse_objective) {
     jcomm_reference(fuse_objective);
+    if (beta_ == 1.0 && n1_enabled_) {
+      n1_numerators();
+      for (int l = 0; l < inner_steps; ++l)
+        for (int n = 0; n < N_; ++n) jcomm_inner_n1(n);
+      return;
+    }
     for (int l = 0; l < inner_steps; ++l)
       for (int n = 0; n < N_; ++n) jcomm_inner(n);
   }
+  void set_n1(bool on) { n1_enabled_ = on; }
 
   const T* x() const { return x_; }
   unsigned* flag_ptr() const { return flags_; }
@@ -498,6 +572,11 @@ class CpEngine {
   void launch_recon(const ReconParams<T>& p) {
     constexpr int KT2 = (sizeof(T) == 4 && RP <= 32) ? 2 : 1;
     const dim3 grid(recon_grid_);
+    if (recon_v3_) {
+      constexpr int K3 = sizeof(T) == 4 ? (RP <= 16 ? 4 : RP <= 32 ? 2 : 1) : (RP <= 16 ? 2 : 1);
+      launch_dyn(recon3_kernel<T, RP, K3>, grid, dim3(128), R3Smem<T, RP, K3>::total, p);
+      return;
+    }
     if (recon_kt() == 2) {
       if constexpr (KT2 == 2) {
         if (recon_tpb() == 256) launch_dyn(recon2_kernel<T, RP, 2, 256>, grid, dim3(256), recon2_smem<T, 2, 256>(), p);
@@ -546,8 +625,30 @@ class CpEngine {
     else launch_c2<NS, RC, KT, 128>(p, grid);
   }
 
+  template <int NS, int RC, int KT>
+  void launch_c3(const ContractParams<T, NS>& p, int grid) {
+    launch_dyn(contract3_kernel<T, RC, KT, NS>, dim3(grid), dim3(NS * 128), C3Smem<T, RC, KT, NS>::total, p);
+  }
+
   template <int NS>
   void launch_contract(const ContractParams<T, NS>& p, const Plan& pl, int grid) {
+    if (pl.v3) {
+      if constexpr (sizeof(T) == 4) {
+        switch (pl.RC) {
+          case 8: launch_c3<NS, 8, 4>(p, grid); break;
+          case 16: launch_c3<NS, 16, 4>(p, grid); break;
+          case 32: launch_c3<NS, 32, 4>(p, grid); break;
+          default: launch_c3<NS, 64, 1>(p, grid); break;
+        }
+      } else {
+        switch (pl.RC) {
+          case 8: launch_c3<NS, 8, 2>(p, grid); break;
+          case 16: launch_c3<NS, 16, 2>(p, grid); break;
+          default: launch_c3<NS, 32, 2>(p, grid); break;
+        }
+      }
+      return;
+    }
     if constexpr (sizeof(T) == 4) {
       if (pl.KT == 2) {
         switch (pl.RC) {
@@ -592,9 +693,12 @@ class CpEngine {
   T* partA_ = nullptr;
   double* partB_ = nullptr;
   double* partAd_ = nullptr;
+  double* n1num_ = nullptr;
+  bool n1_enabled_ = true;
   unsigned* flags_;
   int* counter_;
-  int recon_grid_;
+  int recon_grid_ = 0;
+  bool recon_v3_ = false;
 };
 
 }  // namespace ntfg

@@ -373,4 +373,5 @@ constexpr size_t contract2_smem() {
          size_t(NS) * (TPS / 32) * RC * sizeof(double);
 }
 
+
 }  // namespace ntfg

@@ -288,6 +288,8 @@ void tucker_step(Context& c, int prec, int kind, double beta, double eps, uint64
   if (kind == 3 && inner < 1) throw Error(NTFG_ERR_DOMAIN, "jcomm_tucker_outer_step: inner_steps must be >= 1");
   if ((kind == 4 || kind == 5) && (!ref_core || !ref_factors))
     throw Error(NTFG_ERR_SHAPE, "reference model required");
+  if ((kind == 6 && !ref_core) || (kind == 7 && (!ref_factors || mode >= order)))
+    throw Error(NTFG_ERR_SHAPE, "anchor required");
   NTFG_TDISPATCH(prec, {
     with_tucker<T>(c, order, dims, ranks, beta, eps, [&](TuckerEngine<T>& e) {
       e.stream().set_x(x, 0, NTFG_HOST);
@@ -301,6 +303,17 @@ void tucker_step(Context& c, int prec, int kind, double beta, double eps, uint64
           check_positive(core, size_t(e.core_size()));
           e.jcomm_outer(int(inner), false);
           break;
+        case 6: {  // block_core_update_anchored: ref_core is the anchor core
+          c.h2d(e.anchors(), ref_core, size_t(e.core_size()) * sizeof(double));
+          e.block_core(e.anchors(), false);
+          break;
+        }
+        case 7: {  // block_factor_update_anchored: ref_factors is the anchor block of `mode`
+          double* anc = e.anchors() + e.core_size() + e.factor_offset(int(mode));
+          c.h2d(anc, ref_factors, size_t(dims[mode] * ranks[mode]) * sizeof(double));
+          e.block_factor(int(mode), anc);
+          break;
+        }
         case 4:
         case 5:
           e.set_ref_host(ref_core, ref_factors);

@@ -81,6 +81,7 @@ class TuckerEngine {
   double* model() const { return GA_; }
   double* anchors() const { return anch_; }
   double* refs() const { return ref_; }
+  int64_t factor_offset(int m) const { return foff_[m]; }
 
   void set_model_host(const double* core, const double* factors) {
     c_.h2d(GA_, core, size_t(Jtot_) * sizeof(double));
