@@ -239,6 +239,26 @@ void cp_jcomm_reference(Context& c, int prec, double beta, double eps, uint32_t 
       e.set_x(x, 0, NTFG_HOST);
       e.set_factors_host(factors);
       e.jcomm_reference(false);
+      if (e.tc()) {  // bf16 hi/lo planes: return hi + lo (the values the contraction uses)
+        const int64_t E = e.entries();
+        double* tmp = c.buf<double>("step.join", size_t(E));
+        const int grid = int(std::min<int64_t>(ceil_div(E, 256), 4096));
+        join_planes_kernel<<<grid, 256, 0, c.stream>>>(static_cast<const __nv_bfloat16*>(e.plane(0)),
+                                                       static_cast<const __nv_bfloat16*>(e.plane(1)), E, tmp);
+        NTFG_LAUNCHED(c);
+        c.d2h(p_out, tmp, size_t(E) * sizeof(double));
+        c.sync();
+        if (beta == 1.0) {
+          for (int64_t i = 0; i < E; ++i) q_out[i] = 1.0;
+        } else {
+          join_planes_kernel<<<grid, 256, 0, c.stream>>>(static_cast<const __nv_bfloat16*>(e.plane(2)),
+                                                         static_cast<const __nv_bfloat16*>(e.plane(3)), E, tmp);
+          NTFG_LAUNCHED(c);
+          c.d2h(q_out, tmp, size_t(E) * sizeof(double));
+          c.sync();
+        }
+        return;
+      }
       std::vector<T> h(size_t(e.entries()));
       c.d2h(h.data(), e.p(), h.size() * sizeof(T));
       c.sync();
@@ -262,8 +282,20 @@ void cp_jcomm_inner_update(Context& c, int prec, double beta, double eps, uint32
     with_engine<T>(c, prec, order, dims, rank, beta, eps, [&](CpEngine<T>& e) {
       e.set_factors_host(current);
       c.h2d(e.Aref_all(), ref, e.factor_doubles() * sizeof(double));
-      e.upload_convert(e.p(), p, 0, NTFG_HOST, e.entries());
-      if (beta != 1.0) e.upload_convert(e.q(), q, 0, NTFG_HOST, e.entries());
+      if (e.tc()) {
+        const int64_t E = e.entries();
+        double* tmp = c.buf<double>("step.join", size_t(E));
+        const int grid = int(std::min<int64_t>(ceil_div(E, 256), 4096));
+        for (int w = 0; w < (beta != 1.0 ? 2 : 1); ++w) {
+          c.h2d(tmp, w == 0 ? p : q, size_t(E) * sizeof(double));
+          split_planes_kernel<<<grid, 256, 0, c.stream>>>(tmp, E, static_cast<__nv_bfloat16*>(e.plane(2 * w)),
+                                                          static_cast<__nv_bfloat16*>(e.plane(2 * w + 1)));
+          NTFG_LAUNCHED(c);
+        }
+      } else {
+        e.upload_convert(e.p(), p, 0, NTFG_HOST, e.entries());
+        if (beta != 1.0) e.upload_convert(e.q(), q, 0, NTFG_HOST, e.entries());
+      }
       const int64_t F = int64_t(e.factor_doubles());
       chi_all_kernel<<<int(ceil_div(F, 256)), 256, 0, c.stream>>>(
           e.A_all(), e.Aref_all(), F, beta, e.chi1_all(), e.chi2_all(), e.flags());

@@ -8,6 +8,7 @@
 // captured once into a CUDA graph by the fit driver.
 #pragma once
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <vector>
@@ -15,6 +16,7 @@
 #include "cp_kernels.cuh"
 #include "engine.cuh"
 #include "stream3_kernels.cuh"
+#include "tc_contract.cuh"
 
 namespace ntfg {
 
@@ -72,6 +74,7 @@ class CpEngine {
     numden_ = c_.buf<double>("cp.numden", size_t(2) * max_dim() * R_);
     // objective partials: one per recon CTA (grid depends on the kernel variant)
     objpart_ = c_.buf<double>("cp.objpart", size_t(std::max(recon_grid(false), recon_grid(true))));
+    tc_ = decide_tc();
   }
 
   int order() const { return N_; }
@@ -126,8 +129,32 @@ class CpEngine {
 
   // ---- scratch for P / Q -----------------------------------------------------
   void ensure_pq() {
+    if (tc_) {
+      if (!planes_[0]) {
+        planes_[0] = c_.bufs.get("cp.ph", size_t(E_) * 2);
+        planes_[1] = c_.bufs.get("cp.pl", size_t(E_) * 2);
+      }
+      if (!planes_[2] && beta_ != 1.0) {
+        planes_[2] = c_.bufs.get("cp.qh", size_t(E_) * 2);
+        planes_[3] = c_.bufs.get("cp.ql", size_t(E_) * 2);
+      }
+      return;
+    }
     if (!p_) p_ = c_.buf<T>("cp.p", size_t(E_));
     if (!q_ && beta_ != 1.0) q_ = c_.buf<T>("cp.q", size_t(E_));
+  }
+
+  // weights of the model `fac` into the P/Q storage of this engine
+  // (fp32/fp64 arrays, or bf16 hi/lo planes on the tensor-core path)
+  void recon_pq(const double* const* fac, const T* alast, bool write_q, bool objective) {
+    ensure_pq();
+    if (tc_) {
+      planes_out_ = true;
+      recon(fac, alast, nullptr, nullptr, objective);
+      planes_out_ = false;
+    } else {
+      recon(fac, alast, p_, write_q ? q_ : nullptr, objective);
+    }
   }
   T* p() { ensure_pq(); return p_; }
   // Q buffer even at beta = 1 (the Tucker path contracts Q == 1 densely, as
@@ -189,12 +216,14 @@ class CpEngine {
     p.qout = qout;
     p.xhout = xhout;
     p.htab = htab;
+    if (planes_out_)
+      for (int i = 0; i < 4; ++i) p.planes[i] = planes_[i];
     p.obj = objective ? objpart_ : nullptr;
     p.flags = flags_;
     p.beta = beta_;
     p.eps = eps_;
     p.bk = bk_;
-    const bool v3 = rows_tma_ok(x_) && (!pout || rows_tma_ok(pout)) && (!qout || rows_tma_ok(qout));
+    const bool v3 = (rows_tma_ok(x_) && (!pout || rows_tma_ok(pout)) && (!qout || rows_tma_ok(qout))) || planes_out_;
     recon_grid_ = recon_grid(v3);
     recon_v3_ = v3;
     p.ktiles = int(ceil_div(g_.K, v3 ? int64_t(128) * recon_kt3() : int64_t(recon_tpb()) * recon_kt()));
@@ -231,7 +260,95 @@ class CpEngine {
     const T* src;
     const double* fac[kMaxOrder];
     const double* mtab = nullptr;  // case A row table (Tucker partial reconstruction)
+    int plane = -1;                // tensor-core path: 0 = P planes, 1 = Q planes
   };
+
+  // ---- tensor-core K3 (tc_contract.cuh) -------------------------------------------
+  // Eligible: fp32 build, K a multiple of 128 up to 512, rank <= 64 with the
+  // double-buffered accumulator fitting TMEM, 16-row TMA boxes for every mode.
+  bool decide_tc() const {
+    if (sizeof(T) != 4 || !tc_allowed_) return false;
+    if (const char* e = std::getenv("NTFG_DISABLE_TC")) if (e[0] == '1') return false;
+    if (g_.K % 128 != 0 || g_.K > 512 || R_ > 64 || g_.rows >= (int64_t(1) << 31)) return false;
+    const int N = tc_n();
+    if (2 * (g_.K / 128) * N > 256) return false;
+    for (int n = 0; n < N_ - 1; ++n) {
+      int64_t Bn = 1;
+      for (int m = n + 1; m < N_ - 1; ++m) Bn *= g_.dims[m];
+      if (!(Bn % 16 == 0 || Bn == 1 || Bn == 2 || Bn == 4 || Bn == 8)) return false;
+    }
+    return true;
+  }
+  int tc_n() const { return R_ <= 16 ? 16 : R_ <= 32 ? 32 : 64; }
+  bool tc() const { return tc_; }
+  void disable_tc() { tc_allowed_ = false; tc_ = false; }
+  void* plane(int i) { ensure_pq(); return planes_[i]; }
+
+  void tc_contract(int n, int ns, const Stream* st, int64_t& units_out, int64_t& S_out) {
+    const bool caseA = (n == N_ - 1);
+    TcParams p{};
+    p.g = g_;
+    p.n = n;
+    p.R = int(R_);
+    p.RP = RP_;
+    p.N = tc_n();
+    p.ns = ns;
+    p.mt = int(g_.K / 128);
+    p.caseA = caseA;
+    const int64_t In = g_.dims[n];
+    TcMaps maps{};
+    int64_t mapB, mapI = 1, mapA = 1;
+    if (caseA) {
+      const int64_t target = std::min<int64_t>(ceil_div(g_.rows, kTcRows), int64_t(c_.sm_count));
+      p.chunk = ceil_div(ceil_div(g_.rows, target), kTcRows) * kTcRows;
+      p.units = ceil_div(g_.rows, p.chunk);
+      p.S = 1;
+      p.An = 1;
+      p.Bn = g_.rows;
+      p.boxB = kTcRows;
+      p.boxA = 1;
+      mapB = g_.rows;
+    } else {
+      int64_t An = 1, Bn = 1;
+      for (int m = 0; m < n; ++m) An *= g_.dims[m];
+      for (int m = n + 1; m < N_ - 1; ++m) Bn *= g_.dims[m];
+      const int64_t tot = An * Bn;
+      const int64_t S = std::max<int64_t>(1, std::min<int64_t>(ceil_div(int64_t(4) * c_.sm_count, In),
+                                                               ceil_div(tot, kTcRows)));
+      p.chunk = ceil_div(ceil_div(tot, S), kTcRows) * kTcRows;
+      p.S = ceil_div(tot, p.chunk);
+      p.units = In * p.S;
+      p.An = An;
+      p.Bn = Bn;
+      p.boxB = int(Bn >= kTcRows ? kTcRows : Bn);
+      p.boxA = kTcRows / p.boxB;
+      mapB = Bn;
+      mapI = In;
+      mapA = An;
+    }
+    p.fB.init(p.Bn);
+    for (int s = 0; s < ns; ++s) {
+      for (int m = 0; m < N_; ++m) p.mfac[s][m] = st[s].fac[m];
+      p.lastfac[s] = st[s].fac[N_ - 1];
+      for (int h = 0; h < 2; ++h)
+        if (!tc::make_plane_map(&maps.m[s][h], planes_[2 * st[s].plane + h], g_.K, mapB, mapI, mapA, p.boxB,
+                                p.boxA))
+          throw Error(NTFG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    }
+    p.partA = reinterpret_cast<float*>(partA_);
+    p.partB = partB_;
+    const int cols = ns * p.mt * p.N;
+    p.dbuf = 2 * cols <= 512 ? 1 : 0;
+    int alloc = 32;
+    while (alloc < (p.dbuf ? 2 : 1) * cols) alloc *= 2;
+    p.tmem_cols = alloc;
+    const int grid = int(std::min<int64_t>(p.units, int64_t(c_.sm_count)));
+    if (p.N == 16) launch_dyn(tc_contract_kernel<16>, dim3(grid), dim3(320), TcSmem<16>::total, maps, p);
+    else if (p.N == 32) launch_dyn(tc_contract_kernel<32>, dim3(grid), dim3(320), TcSmem<32>::total, maps, p);
+    else launch_dyn(tc_contract_kernel<64>, dim3(grid), dim3(320), TcSmem<64>::total, maps, p);
+    units_out = p.units;
+    S_out = p.S;
+  }
 
   struct Plan {
     bool caseA, v3;
@@ -301,17 +418,20 @@ class CpEngine {
     if (!partA_) prealloc(2);
     bool v3 = true;
     for (int s2 = 0; s2 < ns; ++s2) v3 = v3 && rows_tma_ok(st[s2].src);
+    const bool use_tc = tc_ && st[0].plane >= 0;
     const Plan pl = plan(n, v3);
     const bool caseA = pl.caseA;
     const int RC = pl.RC;
     const int ktiles = pl.ktiles;
-    const int64_t In = pl.In, units = pl.units, S = pl.S, An = pl.An, Bn = pl.Bn;
+    const int64_t In = pl.In, An = pl.An, Bn = pl.Bn;
+    int64_t units = pl.units, S = pl.S;
     const int grid = pl.grid;
     T* partA = caseA ? partA_ : nullptr;
     double* partB = caseA ? nullptr : partB_;
 
     const int ph = c_.prof_begin(1);
-    for (int r0 = 0; r0 < R_; r0 += RC) {
+    if (use_tc) tc_contract(n, ns, st, units, S);
+    for (int r0 = 0; r0 < R_ && !use_tc; r0 += RC) {
       if (ns == 2) {
         ContractParams<T, 2> p{};
         fill_contract(p, n, r0, caseA, units, S, An, Bn, partA, partB, ktiles, st, 2);
@@ -406,13 +526,16 @@ class CpEngine {
       stage(anchor, stage_anchor_);
       alast = stage_anchor_;
     }
-    ensure_pq();
-    recon(fac, alast, p_, beta_ != 1.0 ? q_ : nullptr, objective);
+    recon_pq(fac, alast, beta_ != 1.0, objective);
     const bool closed = beta_ == 1.0;
     if (closed) colprod(fac, n);
     Stream st[2];
     st[0].src = p_;
     st[1].src = q_;
+    if (tc_) {
+      st[0].plane = 0;
+      st[1].plane = 1;
+    }
     for (int m = 0; m < N_; ++m) st[0].fac[m] = st[1].fac[m] = fac[m];
     contract_and_update(n, closed ? 1 : 2, st, closed, anchor, A(n), nullptr, nullptr, nullptr,
                         n == N_ - 1 ? stage_ : nullptr);
@@ -435,8 +558,7 @@ class CpEngine {
     c_.d2d(chi2_, A_, bytes);
     const double* fac[kMaxOrder];
     for (int m = 0; m < N_; ++m) fac[m] = A(m);
-    ensure_pq();
-    recon(fac, stage_, p_, beta_ != 1.0 ? q_ : nullptr, objective);
+    recon_pq(fac, stage_, beta_ != 1.0, objective);
   }
 
   // jcomm_inner_update (cp.cpp:210-229)
@@ -448,6 +570,10 @@ class CpEngine {
     Stream st[2];
     st[0].src = p_;
     st[1].src = q_;
+    if (tc_) {
+      st[0].plane = 0;
+      st[1].plane = 1;
+    }
     for (int m = 0; m < N_; ++m) {
       st[0].fac[m] = chi1_ + off_[m];
       st[1].fac[m] = chi2_ + off_[m];
@@ -466,6 +592,7 @@ class CpEngine {
     Stream st[2];
     st[0].src = p_;
     st[1].src = p_;
+    if (tc_) st[0].plane = st[1].plane = 0;
     for (int m = 0; m < N_; ++m) st[0].fac[m] = st[1].fac[m] = Aref_ + off_[m];
     for (int n = 0; n < N_; ++n) {
       contract_and_update(n, 1, st, true, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 1);
@@ -552,8 +679,8 @@ class CpEngine {
   }
 
  private:
-  template <typename K2, typename P>
-  void launch_dyn(K2 kern, dim3 grid, dim3 block, size_t smem, const P& p) {
+  template <typename K2, typename... P>
+  void launch_dyn(K2 kern, dim3 grid, dim3 block, size_t smem, const P&... p) {
     // one attribute call per kernel (keyed by its address: many kernels share
     // a signature, so a per-signature static would miss all but the first)
     static std::mutex mu;
@@ -564,7 +691,7 @@ class CpEngine {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
                    "cudaFuncSetAttribute");
     }
-    kern<<<grid, block, smem, c_.stream>>>(p);
+    kern<<<grid, block, smem, c_.stream>>>(p...);
     NTFG_LAUNCHED(c_);
   }
 
@@ -695,6 +822,10 @@ class CpEngine {
   double* partAd_ = nullptr;
   double* n1num_ = nullptr;
   bool n1_enabled_ = true;
+  bool tc_ = false;
+  bool tc_allowed_ = true;
+  bool planes_out_ = false;
+  void* planes_[4] = {nullptr, nullptr, nullptr, nullptr};
   unsigned* flags_;
   int* counter_;
   int recon_grid_ = 0;

@@ -98,6 +98,7 @@ struct ReconParams {
   T* pout;                       // nullable
   T* qout;                       // nullable
   T* xhout;                      // nullable: materialised Xhat (cp_reconstruct API only)
+  void* planes[4];               // nullable: bf16 hi/lo planes of P and Q (tensor-core K3)
   double* obj;                   // per-CTA objective partial (nullable)
   unsigned* flags;               // domain flags (nullable)
   double beta, eps;

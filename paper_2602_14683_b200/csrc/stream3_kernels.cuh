@@ -13,6 +13,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <cuda_bf16.h>
+
 #include "stream_kernels.cuh"
 
 namespace ntfg {
@@ -75,6 +77,22 @@ template <> __device__ __forceinline__ float acc_fma<float>(float s, double m, f
 template <> __device__ __forceinline__ double acc_fma<double>(double s, double m, double g) { return fma(s, m, g); }
 
 constexpr int kPre = 3;  // row-mode factor values prefetched per item
+
+// p ~= hi + lo with hi = RN_bf16(p), lo = RN_bf16(p - hi), except that lo is
+// rounded toward zero when RN would make hi + lo an exact bf16 tie: then
+// RN_bf16(hi + lo) == hi always, so planes written here survive the fp64
+// round trip of the step-level API (join -> host -> split) bit for bit.
+__device__ __forceinline__ void bf16_split_stable(float p, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(p);
+  const float hf = __bfloat162float(hi);
+  const float d = p - hf;  // exact
+  __nv_bfloat16 l = __float2bfloat16_rn(d);
+  // half an ulp of hi on the side of d (below a power of two the ulp halves)
+  float half = __int_as_float(__float_as_int(hf) & 0x7f800000) * 0.00390625f;  // 2^(e-8)
+  if ((__float_as_int(hf) & 0x007fffff) == 0 && ((d < 0.f) == (hf > 0.f))) half *= 0.5f;
+  if (hf != 0.f && fabsf(__bfloat162float(l)) == half && fabsf(d) != half) l = __float2bfloat16_rz(d);
+  lo = l;
+}
 
 // Per-thread prefetch of row-vector entries (fp64 factor gathers), one stage ahead.
 template <int ITEMS>
@@ -454,10 +472,20 @@ static __global__ void __launch_bounds__(128) recon3_kernel(const ReconParams<T>
 #pragma unroll
       for (int kk = 0; kk < KT; ++kk) {
         if (p.xhout) p.xhout[row * K + k0 + kk] = xhp[kk];
-        if (p.pout) weights_entry(xv[kk], xhp[kk], p.bk, p.beta, p.eps, pw[kk], qw[kk]);
+        if (p.pout || p.planes[0]) weights_entry(xv[kk], xhp[kk], p.bk, p.beta, p.eps, pw[kk], qw[kk]);
         if (p.obj) obj += objective_term<T>(xv[kk], xhp[kk], p.bk, p.beta, bad);
       }
-      if (p.pout) {
+      if (p.planes[0]) {  // tensor-core storage: bf16 hi/lo planes of P and Q
+        __nv_bfloat16* ph = static_cast<__nv_bfloat16*>(p.planes[0]) + row * K + k0;
+        __nv_bfloat16* pl = static_cast<__nv_bfloat16*>(p.planes[1]) + row * K + k0;
+        __nv_bfloat16* qh = static_cast<__nv_bfloat16*>(p.planes[2]) + row * K + k0;
+        __nv_bfloat16* ql = static_cast<__nv_bfloat16*>(p.planes[3]) + row * K + k0;
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk) {
+          bf16_split_stable(float(pw[kk]), ph[kk], pl[kk]);
+          if (p.planes[2]) bf16_split_stable(float(qw[kk]), qh[kk], ql[kk]);
+        }
+      } else if (p.pout) {
         *reinterpret_cast<typename VecT<T, KT>::type*>(p.pout + row * K + k0) =
             *reinterpret_cast<const typename VecT<T, KT>::type*>(pw);
         if (p.qout)

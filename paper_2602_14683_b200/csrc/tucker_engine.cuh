@@ -28,6 +28,7 @@ class TuckerEngine {
                double eps, const ntfg_shard* shard)
       : c_(c), N_(int(order)), L_(int(order) - 1), beta_(beta), eps_(eps),
         s_(c, order, dims, int64_t(ranks[order - 1]), beta, eps, shard) {
+    s_.disable_tc();  // Tucker streams contract fp32 P/Q with the row-table kernels
     gamma_ = gamma_of(beta);
     I_.resize(N_);
     J_.resize(N_);

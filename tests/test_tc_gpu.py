@@ -1,0 +1,77 @@
+"""Tensor-core contraction path (tc_contract.cuh; fp32 build, K % 128 == 0).
+
+Parity against the fp64 oracle at the fp32 tolerances (1e-4 factors, 1e-5
+trace), against the CUDA-core path (NTFG_DISABLE_TC=1), the bitwise
+first-inner == block property, and the step-level P~/Q~ round trip through
+the bf16 hi/lo planes.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2602_14683_b200 as ntf
+from oracle import ntf_oracle as O
+
+pytestmark = pytest.mark.gpu
+EPS = 1e-12
+
+
+def problem(dims, rank, seed):
+    rng = np.random.default_rng(seed)
+    truth = [rng.random((d, rank)) for d in dims]
+    x = O.cp_reconstruct(truth) * rng.gamma(10.0, 0.1, size=dims)
+    init = [0.1 + rng.random((d, rank)) for d in dims]
+    return x, init
+
+
+def relm(a, b):
+    return max(O.rel_err(u, v) for u, v in zip(a, b))
+
+
+@pytest.mark.parametrize("algo", ["bcomm", "jcomm"])
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 1.5])
+@pytest.mark.parametrize("dims,rank", [((24, 16, 128), 8), ((6, 4, 8, 256), 5), ((20, 17, 128), 32)])
+def test_tc_fit_matches_oracle(algo, beta, dims, rank):
+    x, init = problem(dims, rank, 3)
+    cfg = ntf.FitConfig(beta=beta, rank=rank, max_iters=20, inner_steps=3, precision="f32")
+    fit = ntf.bcomm_fit if algo == "bcomm" else ntf.jcomm_fit
+    res = fit(x, init, cfg)
+    ofit = O.bcomm_fit if algo == "bcomm" else O.jcomm_fit
+    om, otr = ofit(x, init, O.FitConfig(beta=beta, rank=rank, max_iters=20, inner_steps=3))
+    assert relm(res.model, om) < 1e-4
+    assert O.rel_err([t.loss for t in res.trace], [t[2] for t in otr]) < 1e-5
+
+
+@pytest.mark.parametrize("beta", [0.5, 1.0])
+def test_tc_matches_cuda_core_path(beta, monkeypatch):
+    x, init = problem((32, 16, 256), 16, 5)
+    cfg = ntf.FitConfig(beta=beta, rank=16, max_iters=10, inner_steps=5, precision="f32")
+    a = ntf.jcomm_fit(x, init, cfg)
+    monkeypatch.setenv("NTFG_DISABLE_TC", "1")
+    b = ntf.jcomm_fit(x, init, cfg)
+    assert relm(a.model, b.model) < 1e-4
+    assert O.rel_err([t.loss for t in a.trace], [t[2] if isinstance(t, tuple) else t.loss for t in b.trace]) < 1e-6
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 1.5])
+def test_tc_first_joint_inner_equals_block_bitwise(beta):
+    x, f = problem((16, 8, 128), 4, 7)
+    ctx = ntf.make_jcomm_reference(f, x, beta, EPS, precision="f32")
+    for mode in range(3):
+        joint = ntf.jcomm_inner_update(f, ctx, mode, beta, EPS, precision="f32")
+        block = ntf.bcomm_block_update(f, mode, x, beta, EPS, precision="f32")
+        assert np.array_equal(joint[mode], block[mode]), mode
+
+
+def test_tc_reference_planes_round_trip():
+    x, f = problem((16, 8, 128), 4, 9)
+    ctx = ntf.make_jcomm_reference(f, x, 0.5, EPS, precision="f32")
+    _, op, oq = O.make_jcomm_reference(f, x, 0.5, EPS)
+    # hi + lo bf16 planes: ~2^-17 relative
+    assert O.rel_err(ctx.p / np.maximum(op, 1e-30), np.ones_like(op)) < 2e-5
+    assert O.rel_err(ctx.q / oq, np.ones_like(oq)) < 2e-5
+    cur = [a * 1.1 for a in f]
+    got = ntf.jcomm_inner_update(cur, ctx, 1, 0.5, EPS, precision="f32")
+    want = O.jcomm_inner_update(cur, (f, op, oq), 1, 0.5, EPS)
+    assert relm(got, want) < 1e-4
