@@ -90,11 +90,25 @@ class CpEngine {
     const bool want_f32 = sizeof(T) == 4;
     if (location == NTFG_DEVICE && ((dtype == 1) == want_f32)) {
       x_ = static_cast<const T*>(x);
+      compute_xconst();
       return;
     }
     T* dst = c_.buf<T>("cp.x", size_t(E_));
     upload_convert(dst, x, dtype, location, E_);
     x_ = dst;
+    compute_xconst();
+  }
+
+  // x-only objective constant for the tensor-core recon (see xconst_kernel);
+  // computed when the data arrives, outside any captured graph.
+  bool split_objective() const { return tc_ && (bk_ == kBetaHalf || bk_ == kBeta3Half || bk_ == kBetaGeneric); }
+  void compute_xconst() {
+    if (!split_objective()) return;
+    if (!xconst_) xconst_ = c_.buf<double>("cp.xconst", 1 + kXconstGrid);
+    xconst_kernel<T><<<kXconstGrid, 256, 0, c_.stream>>>(x_, E_, beta_, xconst_ + 1);
+    NTFG_LAUNCHED(c_);
+    xconst_finish_kernel<<<1, 256, 0, c_.stream>>>(xconst_ + 1, kXconstGrid, 1.0 / (beta_ * (beta_ - 1.0)), xconst_);
+    NTFG_LAUNCHED(c_);
   }
 
   void upload_convert(T* dst, const void* src, int dtype, int location, int64_t n) {
@@ -223,6 +237,7 @@ class CpEngine {
     p.beta = beta_;
     p.eps = eps_;
     p.bk = bk_;
+    obj_split_ = planes_out_ && split_objective();
     const bool v3 = (rows_tma_ok(x_) && (!pout || rows_tma_ok(pout)) && (!qout || rows_tma_ok(qout))) || planes_out_;
     recon_grid_ = recon_grid(v3);
     recon_v3_ = v3;
@@ -242,13 +257,15 @@ class CpEngine {
   void finish_objective() {
     const double inv = 1.0 / double(E_global_);
     if (sharded_) {
-      objective_finalize_kernel<<<1, 256, 0, c_.stream>>>(objpart_, recon_grid_, inv, losses_, counter_, raw_);
+      objective_finalize_kernel<<<1, 256, 0, c_.stream>>>(objpart_, recon_grid_, inv, losses_, counter_, raw_,
+                                                           obj_split_ ? xconst_ : nullptr);
       NTFG_LAUNCHED(c_);
       allreduce(raw_, 1);
       objective_scale_kernel<<<1, 1, 0, c_.stream>>>(raw_, inv, losses_, counter_);
       NTFG_LAUNCHED(c_);
     } else {
-      objective_finalize_kernel<<<1, 256, 0, c_.stream>>>(objpart_, recon_grid_, inv, losses_, counter_, nullptr);
+      objective_finalize_kernel<<<1, 256, 0, c_.stream>>>(objpart_, recon_grid_, inv, losses_, counter_, nullptr,
+                                                           obj_split_ ? xconst_ : nullptr);
       NTFG_LAUNCHED(c_);
     }
   }
@@ -329,7 +346,13 @@ class CpEngine {
     p.fB.init(p.Bn);
     for (int s = 0; s < ns; ++s) {
       for (int m = 0; m < N_; ++m) p.mfac[s][m] = st[s].fac[m];
-      p.lastfac[s] = st[s].fac[N_ - 1];
+      if (!caseA) {
+        if (!lastT_) lastT_ = c_.buf<float>("cp.lastT", size_t(2) * g_.K * R_);
+        float* lt = lastT_ + size_t(s) * g_.K * R_;
+        transpose_kr_kernel<<<int(ceil_div(g_.K * R_, 256)), 256, 0, c_.stream>>>(st[s].fac[N_ - 1], g_.K, int(R_), lt);
+        NTFG_LAUNCHED(c_);
+        p.lastfac[s] = lt;
+      }
       for (int h = 0; h < 2; ++h)
         if (!tc::make_plane_map(&maps.m[s][h], planes_[2 * st[s].plane + h], g_.K, mapB, mapI, mapA, p.boxB,
                                 p.boxA))
@@ -404,6 +427,7 @@ class CpEngine {
     partB_ = c_.buf<double>("cp.partB", std::max<size_t>(b, 1));
     partAd_ = c_.buf<double>("cp.partAd", std::max<size_t>(a / 8 + size_t(ns) * g_.K * RP_, 1));
     if (beta_ == 1.0) n1num_ = c_.buf<double>("cp.n1num", factor_doubles() + size_t(max_dim()) * R_);
+    if (tc_) lastT_ = c_.buf<float>("cp.lastT", size_t(2) * g_.K * R_);
     ensure_pq();
   }
 
@@ -701,6 +725,18 @@ class CpEngine {
     const dim3 grid(recon_grid_);
     if (recon_v3_) {
       constexpr int K3 = sizeof(T) == 4 ? (RP <= 16 ? 4 : RP <= 32 ? 2 : 1) : (RP <= 16 ? 2 : 1);
+      if constexpr (sizeof(T) == 4) {
+        if (planes_out_ && !p.pout && !p.xhout) {
+          constexpr size_t sm = R3Smem<T, RP, K3>::total;
+          switch (bk_) {
+            case kBeta1: launch_dyn(recon3_kernel<T, RP, K3, kBeta1>, grid, dim3(128), sm, p); return;
+            case kBetaHalf: launch_dyn(recon3_kernel<T, RP, K3, kBetaHalf>, grid, dim3(128), sm, p); return;
+            case kBeta3Half: launch_dyn(recon3_kernel<T, RP, K3, kBeta3Half>, grid, dim3(128), sm, p); return;
+            case kBeta0: launch_dyn(recon3_kernel<T, RP, K3, kBeta0>, grid, dim3(128), sm, p); return;
+            default: launch_dyn(recon3_kernel<T, RP, K3, kBetaGeneric>, grid, dim3(128), sm, p); return;
+          }
+        }
+      }
       launch_dyn(recon3_kernel<T, RP, K3>, grid, dim3(128), R3Smem<T, RP, K3>::total, p);
       return;
     }
@@ -826,10 +862,14 @@ class CpEngine {
   bool tc_allowed_ = true;
   bool planes_out_ = false;
   void* planes_[4] = {nullptr, nullptr, nullptr, nullptr};
+  float* lastT_ = nullptr;
   unsigned* flags_;
   int* counter_;
   int recon_grid_ = 0;
   bool recon_v3_ = false;
+  bool obj_split_ = false;    // last recon used the split objective (needs xconst_)
+  double* xconst_ = nullptr;  // [0] = x-only objective constant, [1..] partials
+  static constexpr int kXconstGrid = 592;
 };
 
 }  // namespace ntfg

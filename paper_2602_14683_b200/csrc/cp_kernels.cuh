@@ -271,7 +271,8 @@ static __global__ void colprod_kernel(const double* colsum, int order, int skip,
 // with raw != nullptr only the unnormalised sum is written (data-parallel
 // fits allreduce it before normalising with objective_scale_kernel).
 static __global__ void objective_finalize_kernel(const double* partials, int n, double inv_entries,
-                                          double* losses, int* counter, double* raw) {
+                                          double* losses, int* counter, double* raw,
+                                          const double* xconst = nullptr) {
   __shared__ double red[256];
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
@@ -282,14 +283,47 @@ static __global__ void objective_finalize_kernel(const double* partials, int n, 
     __syncthreads();
   }
   if (threadIdx.x == 0) {
+    const double tot = xconst ? red[0] + *xconst : red[0];
     if (raw) {
-      *raw = red[0];
+      *raw = tot;
     } else {
       const int c = *counter;
-      losses[c] = red[0] * inv_entries;
+      losses[c] = tot * inv_entries;
       *counter = c + 1;
     }
   }
+}
+
+// x-only part of d_beta summed over the data tensor (fp64, fixed grid ->
+// deterministic): sum x^b / (b (b-1)), for the tensor-core recon's split
+// objective (stream3_kernels.cuh, tc_weights).  Two stages: per-CTA partials
+// then one CTA.
+template <typename T>
+static __global__ void xconst_kernel(const T* x, int64_t n, double beta, double* partials) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    s += fpow64(double(x[i]), beta);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+}
+
+static __global__ void xconst_finish_kernel(double* partials, int n, double scale, double* out) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0] * scale;
 }
 
 static __global__ void objective_scale_kernel(const double* raw, double inv_entries, double* losses,

@@ -79,19 +79,35 @@ template <> __device__ __forceinline__ double acc_fma<double>(double s, double m
 constexpr int kPre = 3;  // row-mode factor values prefetched per item
 
 // p ~= hi + lo with hi = RN_bf16(p), lo = RN_bf16(p - hi), except that lo is
-// rounded toward zero when RN would make hi + lo an exact bf16 tie: then
-// RN_bf16(hi + lo) == hi always, so planes written here survive the fp64
-// round trip of the step-level API (join -> host -> split) bit for bit.
+// rounded toward zero when hi + lo would be a bf16 tie that rounds away from
+// hi: then RN_bf16(hi + lo) == hi always, so planes written here survive the
+// fp64 round trip of the step-level API (join -> host -> split) bit for bit.
+// hi + lo is exact in fp32 (lo only rounds when d spans > 8 bits below hi).
+__device__ __forceinline__ uint32_t bf16x2_bits(__nv_bfloat162 v) { return *reinterpret_cast<uint32_t*>(&v); }
+__device__ __forceinline__ float bf16_lo_f(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16_hi_f(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+// two values at once (packed cvt): element a in the low half, b in the high half
+__device__ __forceinline__ void bf16_split_pair(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const uint32_t hu = bf16x2_bits(__floats2bfloat162_rn(a, b));
+  const float da = a - bf16_lo_f(hu), db = b - bf16_hi_f(hu);  // exact
+  uint32_t lu = bf16x2_bits(__floats2bfloat162_rn(da, db));
+  const uint32_t chk =
+      bf16x2_bits(__floats2bfloat162_rn(bf16_lo_f(hu) + bf16_lo_f(lu), bf16_hi_f(hu) + bf16_hi_f(lu)));
+  if (chk != hu) {  // rare
+    if ((chk ^ hu) & 0xffffu)
+      lu = (lu & 0xffff0000u) | uint32_t(__bfloat16_as_ushort(__float2bfloat16_rz(da)));
+    if ((chk ^ hu) >> 16) lu = (lu & 0xffffu) | (uint32_t(__bfloat16_as_ushort(__float2bfloat16_rz(db))) << 16);
+  }
+  hi = hu;
+  lo = lu;
+}
+
 __device__ __forceinline__ void bf16_split_stable(float p, __nv_bfloat16& hi, __nv_bfloat16& lo) {
-  hi = __float2bfloat16_rn(p);
-  const float hf = __bfloat162float(hi);
-  const float d = p - hf;  // exact
-  __nv_bfloat16 l = __float2bfloat16_rn(d);
-  // half an ulp of hi on the side of d (below a power of two the ulp halves)
-  float half = __int_as_float(__float_as_int(hf) & 0x7f800000) * 0.00390625f;  // 2^(e-8)
-  if ((__float_as_int(hf) & 0x007fffff) == 0 && ((d < 0.f) == (hf > 0.f))) half *= 0.5f;
-  if (hf != 0.f && fabsf(__bfloat162float(l)) == half && fabsf(d) != half) l = __float2bfloat16_rz(d);
-  lo = l;
+  uint32_t h, l;
+  bf16_split_pair(p, 0.f, h, l);
+  hi = __ushort_as_bfloat16((unsigned short)(h & 0xffffu));
+  lo = __ushort_as_bfloat16((unsigned short)(l & 0xffffu));
 }
 
 // Per-thread prefetch of row-vector entries (fp64 factor gathers), one stage ahead.
@@ -331,7 +347,86 @@ struct R3Smem {
   static constexpr size_t total = ring + bars;
 };
 
-template <typename T, int RP, int KT>
+// Tensor-core flavour of the weights tail, one beta kind per instantiation:
+// P~/Q~ straight into the bf16 hi/lo planes, and the objective in its
+// "model part" form -- the x-only part of d_beta (x^b / (b (b-1)) for
+// b not in {0, 1}) is a per-tensor constant summed once in fp64
+// (xconst_kernel) and added by objective_finalize_kernel, so each entry
+// costs a couple of FMAs on top of the weights it shares Q with.
+struct TailConst {
+  float e, b, b1, b2, ib;  // eps, beta, beta-1, beta-2, 1/(beta(beta-1))
+};
+
+template <int BK>
+__device__ __forceinline__ void tc_weights(float x, float y, const TailConst& k, float& pv, float& qv,
+                                           bool obj, float& oacc, unsigned& bad) {
+  const float c = y < k.e ? k.e : y;  // std::max(xhat, eps)
+  // identical formulas to weights_entry(float, ...)
+  if constexpr (BK == kBeta1) {
+    pv = __fdividef(x, c);
+    qv = 1.f;
+  } else if constexpr (BK == kBetaHalf) {
+    const float rs = rsqrtf(c);
+    qv = rs;
+    pv = x * __fdividef(rs, c);
+  } else if constexpr (BK == kBeta3Half) {
+    const float rs = rsqrtf(c);
+    qv = c * rs;
+    pv = x * rs;
+  } else if constexpr (BK == kBeta0) {
+    const float ic = __fdividef(1.f, c);
+    qv = ic;
+    pv = x * ic * ic;
+  } else {
+    const float lg = __log2f(c);
+    qv = exp2f(k.b1 * lg);
+    pv = x * exp2f(k.b2 * lg);
+  }
+  if (!obj) return;
+  if (!(y > 0.f)) bad |= 1u;
+  if (x < 0.f) bad |= 2u;
+  const bool clamped = y < k.e;  // rare: the objective needs xhat itself
+  float t;
+  if constexpr (BK == kBeta1) {
+    t = (x > 0.f ? x * __logf(clamped ? __fdividef(x, y) : pv) : 0.f) - x + y;
+  } else if constexpr (BK == kBeta0) {
+    const float r = clamped ? __fdividef(x, y) : x * qv;
+    t = x == 0.f ? __int_as_float(0x7f800000) : r - __logf(r) - 1.f;
+  } else if constexpr (BK == kBetaHalf) {  // -4 sqrt(x) + 2 y^-.5 (x + y)
+    const float q = clamped ? rsqrtf(y) : qv;
+    t = 2.f * q * (x + y);
+  } else if constexpr (BK == kBeta3Half) {  // x^1.5 / .75 + y^.5 (2y/3 - 2x)
+    const float q = clamped ? y * rsqrtf(y) : qv;
+    t = q * (y * (2.f / 3.f) - 2.f * x);
+  } else {  // x^b / (b (b-1)) + y^(b-1) ((b-1) y - b x) / (b (b-1))
+    const float q = clamped ? exp2f(k.b1 * __log2f(y)) : qv;
+    t = q * (k.b1 * y - k.b * x) * k.ib;
+  }
+  oacc += t;
+}
+
+// bf16 hi/lo stores of KT consecutive weights
+template <int KT>
+__device__ __forceinline__ void store_planes(const float* w, __nv_bfloat16* hi, __nv_bfloat16* lo) {
+  if constexpr (KT == 1) {
+    bf16_split_stable(w[0], hi[0], lo[0]);
+  } else {
+    uint32_t h[KT / 2], l[KT / 2];
+#pragma unroll
+    for (int j = 0; j < KT / 2; ++j) bf16_split_pair(w[2 * j], w[2 * j + 1], h[j], l[j]);
+    if constexpr (KT == 2) {
+      *reinterpret_cast<uint32_t*>(hi) = h[0];
+      *reinterpret_cast<uint32_t*>(lo) = l[0];
+    } else {
+      *reinterpret_cast<uint2*>(hi) = make_uint2(h[0], h[1]);
+      *reinterpret_cast<uint2*>(lo) = make_uint2(l[0], l[1]);
+    }
+  }
+}
+
+// BK = -1: any output set, beta kind at run time.  BK >= 0 (fp32 only):
+// tensor-core planes output for that beta kind, objective optional.
+template <typename T, int RP, int KT, int BK = -1>
 static __global__ void __launch_bounds__(128) recon3_kernel(const ReconParams<T> p) {
   using L = R3Smem<T, RP, KT>;
   using A = typename Acc<T, KT>::type;
@@ -429,6 +524,13 @@ static __global__ void __launch_bounds__(128) recon3_kernel(const ReconParams<T>
 
   double obj = 0.0;
   unsigned bad = 0;
+  TailConst tk;
+  tk.e = float(p.eps);
+  tk.b = float(p.beta);
+  tk.b1 = float(p.beta - 1.0);
+  tk.b2 = float(p.beta - 2.0);
+  tk.ib = float(1.0 / (p.beta * (p.beta - 1.0)));
+  const bool want_obj = p.obj != nullptr;
   for (int d = 0; d < kDepth - 1; ++d) issue(d);
   load_h(0);
   store_h(0, 0);
@@ -468,6 +570,21 @@ static __global__ void __launch_bounds__(128) recon3_kernel(const ReconParams<T>
       T xv[KT];
       *reinterpret_cast<typename VecT<T, KT>::type*>(xv) =
           *reinterpret_cast<const typename VecT<T, KT>::type*>(xrow + size_t(rr) * W);
+      if constexpr (BK >= 0 && sizeof(T) == 4) {
+        float pw[KT], qw[KT];
+        float oacc = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < KT; ++kk)
+          tc_weights<BK>(float(xv[kk]), float(xhp[kk]), tk, pw[kk], qw[kk], want_obj, oacc, bad);
+        if (want_obj) obj += double(oacc);
+        const int64_t off = row * K + k0;
+        store_planes<KT>(pw, static_cast<__nv_bfloat16*>(p.planes[0]) + off,
+                         static_cast<__nv_bfloat16*>(p.planes[1]) + off);
+        if constexpr (BK != kBeta1)
+          store_planes<KT>(qw, static_cast<__nv_bfloat16*>(p.planes[2]) + off,
+                           static_cast<__nv_bfloat16*>(p.planes[3]) + off);
+        continue;
+      }
       T pw[KT], qw[KT];
 #pragma unroll
       for (int kk = 0; kk < KT; ++kk) {

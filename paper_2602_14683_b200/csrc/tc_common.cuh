@@ -128,9 +128,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // ---- host: 5-D tensor map over one bf16 plane viewed as (ki, ko, b, i, a) ----------
 // element (row, k) of the plane with row = a*(In*Bn) + i*Bn + b lives at
-// ((a*In + i)*Bn + b)*K + ko*64 + ki.  Box = (64, 1, boxB, 1, boxA): one
-// 64-column block of boxB*boxA (= 16) rows, landing as a [16][64] bf16 tile
-// with the 128-byte swizzle (two canonical MN-major SW128 atoms along K).
+// ((a*In + i)*Bn + b)*K + ko*64 + ki.  Box = (64, boxB, 1, boxA, K/64): all
+// 64-column blocks of boxB*boxA (= 16) rows, landing as K/64 [16][64] bf16
+// tiles with the 128-byte swizzle (two canonical MN-major SW128 atoms along K
+// each).
 inline bool make_plane_map(CUtensorMap* map, const void* base, int64_t K, int64_t Bn, int64_t In, int64_t An,
                            int boxB, int boxA) {
   using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -144,9 +145,13 @@ inline bool make_plane_map(CUtensorMap* map, const void* base, int64_t K, int64_
       return false;
     encode = reinterpret_cast<Encode>(fn);
   }
-  const cuuint64_t dims[5] = {64, cuuint64_t(K / 64), cuuint64_t(Bn), cuuint64_t(In), cuuint64_t(An)};
-  const cuuint64_t strides[4] = {128, cuuint64_t(K * 2), cuuint64_t(Bn * K * 2), cuuint64_t(In * Bn * K * 2)};
-  const cuuint32_t box[5] = {64, 1, cuuint32_t(boxB), 1, cuuint32_t(boxA)};
+  // the 64-column block index is the SLOWEST box dimension (stride 128 B,
+  // non-monotonic strides are accepted: tools/tc_probe2.cu), so one TMA lands
+  // the whole stage as [K/64][16 rows][64] -- one instruction per plane
+  // instead of K/64.
+  const cuuint64_t dims[5] = {64, cuuint64_t(Bn), cuuint64_t(In), cuuint64_t(An), cuuint64_t(K / 64)};
+  const cuuint64_t strides[4] = {cuuint64_t(K * 2), cuuint64_t(Bn * K * 2), cuuint64_t(In * Bn * K * 2), 128};
+  const cuuint32_t box[5] = {64, cuuint32_t(boxB), 1, cuuint32_t(boxA), cuuint32_t(K / 64)};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -40,7 +40,8 @@ struct TcParams {
   int boxB, boxA;        // TMA box for the 16 rows of a stage
   FastDiv fB;
   const double* mfac[2][kMaxOrder];
-  const double* lastfac[2];
+  const float* lastfac[2];   // case B: last-mode factor transposed to [R][K] in fp32 (coalesced epilogue;
+                             // G itself is an fp32 MMA result, so fp32 F adds ~6e-8 per term)
   float* partA;          // [ns][units][K][RP]
   double* partB;         // [ns][In][S][RP]
   int tmem_cols, dbuf;   // allocation, double-buffered accumulator?
@@ -152,9 +153,7 @@ static __global__ void __launch_bounds__(320, 1)
           }
           for (int s = 0; s < p.ns; ++s)
             for (int plane = 0; plane < 2; ++plane)
-              for (int ko = 0; ko < int(K / 64); ++ko)
-                tc::tma_load_5d(stage_a(slot, s, plane) + size_t(ko) * 2048, &maps.m[s][plane], 0, ko, c2, c3, c4,
-                                &a_full[slot]);
+              tc::tma_load_5d(stage_a(slot, s, plane), &maps.m[s][plane], 0, c2, c3, c4, 0, &a_full[slot]);
         }
       }
     }
@@ -275,36 +274,59 @@ static __global__ void __launch_bounds__(320, 1)
       tc::wait(&acc_full[tb], use & 1u);
       tc::fence_after_sync();
       for (int s = 0; s < p.ns; ++s) {
-        double acc[NMAX];
-        if (!p.caseA)
-          for (int r = 0; r < N; ++r) acc[r] = 0.0;
-        for (int m = 0; m < p.mt; ++m) {
-          const int64_t k = int64_t(m) * 128 + quarter * 32 + lane;
-          for (int c0 = 0; c0 < N; c0 += 32) {
-            uint32_t v[32];
-            tc::tmem_ld32(tmem + (uint32_t(quarter * 32) << 16) + tb * uint32_t(cols_per_buf) +
-                              uint32_t((s * p.mt + m) * N + c0),
-                          v);
-            if (p.caseA) {
-              float* dst = p.partA + ((int64_t(s) * p.units + u) * K + k) * p.RP + c0;
-              for (int r = 0; r < 32 && c0 + r < p.R; ++r) dst[r] = __uint_as_float(v[r]);
-            } else {
-              for (int r = 0; r < 32 && c0 + r < p.R; ++r)
-                acc[c0 + r] += double(__uint_as_float(v[r])) * p.lastfac[s][k * p.R + c0 + r];
+        const uint32_t tcol = tmem + (uint32_t(quarter * 32) << 16) + tb * uint32_t(cols_per_buf) +
+                              uint32_t(s * p.mt * N);
+        if (p.caseA) {
+          for (int m = 0; m < p.mt; ++m) {
+            const int64_t k = int64_t(m) * 128 + quarter * 32 + lane;
+#pragma unroll
+            for (int c0 = 0; c0 < N; c0 += 32) {
+              uint32_t v[32];
+              tc::tmem_ld32(tcol + uint32_t(m * N + c0), v);
+              // one 128-byte row segment per thread, 16-byte stores (columns
+              // R..RP-1 carry the zero B columns' G = 0)
+              float4* dst = reinterpret_cast<float4*>(p.partA + ((int64_t(s) * p.units + u) * K + k) * p.RP + c0);
+#pragma unroll
+              for (int r = 0; r < 32; r += 4)
+                if (c0 + r < p.RP)
+                  dst[r / 4] = make_float4(__uint_as_float(v[r]), __uint_as_float(v[r + 1]),
+                                           __uint_as_float(v[r + 2]), __uint_as_float(v[r + 3]));
             }
           }
+          continue;
         }
-        if (!p.caseA) {
-          for (int r = 0; r < N; ++r) {
-            const double w = warp_sum(acc[r]);
-            if (lane == 0) red[quarter][r] = w;
+        // case B: sum_k F_last(k, r) G(k, r) in fp64, 32 columns at a time
+        // (per column the k order is m ascending, as before)
+#pragma unroll
+        for (int c0 = 0; c0 < N; c0 += 32) {
+          constexpr int CW = N < 32 ? N : 32;
+          double acc[CW];
+#pragma unroll
+          for (int r = 0; r < CW; ++r) acc[r] = 0.0;
+          for (int m = 0; m < p.mt; ++m) {
+            const int64_t k = int64_t(m) * 128 + quarter * 32 + lane;
+            // the last-factor values do not depend on the accumulator: all
+            // loads in flight before the TMEM read (a load->DFMA chain per
+            // column serialises on L2 latency)
+            float lf[CW];
+#pragma unroll
+            for (int r = 0; r < CW; ++r) lf[r] = c0 + r < p.R ? __ldg(p.lastfac[s] + (c0 + r) * K + k) : 0.f;
+            uint32_t v[32];
+            tc::tmem_ld32(tcol + uint32_t(m * N + c0), v);
+#pragma unroll
+            for (int r = 0; r < CW; ++r) acc[r] = fma(double(__uint_as_float(v[r])), double(lf[r]), acc[r]);
           }
-          named_sync(1, 128);
-          if (et < p.R)
-            p.partB[((int64_t(s) * In + itgt) * p.S + split) * p.RP + et] =
-                red[0][et] + red[1][et] + red[2][et] + red[3][et];
-          named_sync(1, 128);
+#pragma unroll
+          for (int r = 0; r < CW; ++r) {
+            const double w = warp_sum(acc[r]);
+            if (lane == 0) red[quarter][c0 + r] = w;
+          }
         }
+        named_sync(1, 128);
+        if (et < p.R)
+          p.partB[((int64_t(s) * In + itgt) * p.S + split) * p.RP + et] =
+              red[0][et] + red[1][et] + red[2][et] + red[3][et];
+        named_sync(1, 128);
       }
       tc::fence_before_sync();
       tc::arrive(&acc_empty[tb]);
@@ -313,6 +335,15 @@ static __global__ void __launch_bounds__(320, 1)
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 9) tc::tmem_dealloc(tmem, uint32_t(p.tmem_cols));
+}
+
+// [K][R] fp64 -> [R][K] fp32, for the coalesced case-B epilogue reads
+static __global__ void transpose_kr_kernel(const double* src, int64_t K, int R, float* dst) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= K * R) return;
+  const int64_t k = i % K;
+  const int r = int(i / K);
+  dst[i] = float(src[k * R + r]);
 }
 
 // host P~/Q~ (fp64) -> bf16 hi/lo planes (step-level uploads).  The split is
