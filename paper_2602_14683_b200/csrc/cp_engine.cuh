@@ -8,6 +8,7 @@
 // captured once into a CUDA graph by the fit driver.
 #pragma once
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <set>
@@ -347,9 +348,10 @@ class CpEngine {
     for (int s = 0; s < ns; ++s) {
       for (int m = 0; m < N_; ++m) p.mfac[s][m] = st[s].fac[m];
       if (!caseA) {
-        if (!lastT_) lastT_ = c_.buf<float>("cp.lastT", size_t(2) * g_.K * R_);
-        float* lt = lastT_ + size_t(s) * g_.K * R_;
-        transpose_kr_kernel<<<int(ceil_div(g_.K * R_, 256)), 256, 0, c_.stream>>>(st[s].fac[N_ - 1], g_.K, int(R_), lt);
+        if (!lastT_) lastT_ = c_.buf<float>("cp.lastT", size_t(2) * g_.K * 64);
+        float* lt = lastT_ + size_t(s) * g_.K * p.N;
+        pad_last_kernel<<<int(ceil_div(g_.K * p.N, 256)), 256, 0, c_.stream>>>(st[s].fac[N_ - 1], g_.K, int(R_),
+                                                                               p.N, lt);
         NTFG_LAUNCHED(c_);
         p.lastfac[s] = lt;
       }
@@ -365,10 +367,31 @@ class CpEngine {
     int alloc = 32;
     while (alloc < (p.dbuf ? 2 : 1) * cols) alloc *= 2;
     p.tmem_cols = alloc;
+    {  // perf experiments only (tools/): role ablation bits, results are wrong when set
+      static const int dbg = [] { const char* e = std::getenv("NTFG_TC_ABLATE"); return e ? std::atoi(e) : 0; }();
+      p.ablate = dbg;
+    }
     const int grid = int(std::min<int64_t>(p.units, int64_t(c_.sm_count)));
+    static const char* trace_path = std::getenv("NTFG_TC_TRACE");  // perf experiments (eager fits only)
+    if (trace_path) {
+      p.trace = reinterpret_cast<unsigned long long*>(c_.bufs.get("cp.tctrace", size_t(grid) * 16 * 8 * 8));
+      NTFG_CUDA(cudaMemsetAsync(p.trace, 0, size_t(grid) * 16 * 8 * 8, c_.stream));
+    }
     if (p.N == 16) launch_dyn(tc_contract_kernel<16>, dim3(grid), dim3(320), TcSmem<16>::total, maps, p);
     else if (p.N == 32) launch_dyn(tc_contract_kernel<32>, dim3(grid), dim3(320), TcSmem<32>::total, maps, p);
     else launch_dyn(tc_contract_kernel<64>, dim3(grid), dim3(320), TcSmem<64>::total, maps, p);
+    if (trace_path) {
+      std::vector<unsigned long long> h(size_t(grid) * 16 * 8);
+      NTFG_CUDA(cudaMemcpyAsync(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost, c_.stream));
+      NTFG_CUDA(cudaStreamSynchronize(c_.stream));
+      if (FILE* f = std::fopen(trace_path, "a")) {
+        std::fprintf(f, "launch n=%d units=%lld S=%lld grid=%d\n", n, (long long)p.units, (long long)p.S, grid);
+        for (size_t i = 0; i < h.size(); i += 8)
+          std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 128, (i / 8) % 16, h[i], h[i + 1],
+                       h[i + 2], h[i + 3], h[i + 4], h[i + 5], h[i + 6], h[i + 7]);
+        std::fclose(f);
+      }
+    }
     units_out = p.units;
     S_out = p.S;
   }
@@ -427,7 +450,7 @@ class CpEngine {
     partB_ = c_.buf<double>("cp.partB", std::max<size_t>(b, 1));
     partAd_ = c_.buf<double>("cp.partAd", std::max<size_t>(a / 8 + size_t(ns) * g_.K * RP_, 1));
     if (beta_ == 1.0) n1num_ = c_.buf<double>("cp.n1num", factor_doubles() + size_t(max_dim()) * R_);
-    if (tc_) lastT_ = c_.buf<float>("cp.lastT", size_t(2) * g_.K * R_);
+    if (tc_) lastT_ = c_.buf<float>("cp.lastT", size_t(2) * g_.K * 64);
     ensure_pq();
   }
 

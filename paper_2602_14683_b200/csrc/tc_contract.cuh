@@ -40,11 +40,13 @@ struct TcParams {
   int boxB, boxA;        // TMA box for the 16 rows of a stage
   FastDiv fB;
   const double* mfac[2][kMaxOrder];
-  const float* lastfac[2];   // case B: last-mode factor transposed to [R][K] in fp32 (coalesced epilogue;
-                             // G itself is an fp32 MMA result, so fp32 F adds ~6e-8 per term)
+  const float* lastfac[2];   // case B: last-mode factor as [K][N] fp32, zero padded past R (G itself
+                             // is an fp32 MMA result, so fp32 F adds ~6e-8 per term)
   float* partA;          // [ns][units][K][RP]
   double* partB;         // [ns][In][S][RP]
   int tmem_cols, dbuf;   // allocation, double-buffered accumulator?
+  int ablate;            // perf experiments (NTFG_TC_ABLATE): 1 no B work, 2 no MMAs, 4 no epilogue work
+  unsigned long long* trace;  // perf experiments: [cta][16 unit iterations][8] clock64 events (nullable)
 };
 
 struct TcMaps {
@@ -167,16 +169,26 @@ static __global__ void __launch_bounds__(320, 1)
         unit_range(u, j0, j1, itgt, split);
         const uint32_t tb = p.dbuf ? (it & 1u) : 0u;
         const uint32_t use = p.dbuf ? (it >> 1) : it;  // uses of this accumulator buffer so far
+        unsigned long long* tr = (p.trace && it < 16) ? p.trace + (size_t(blockIdx.x) * 16 + it) * 8 : nullptr;
+        if (tr) tr[2] = clock64();
         tc::wait(&acc_empty[tb], (use & 1u) ^ 1u);
         tc::fence_after_sync();
+        if (tr) tr[3] = clock64();
+        unsigned long long wa = 0, wb = 0;
         bool first = true;
         for (int64_t j = j0; j < j1; j += kTcRows, ++q) {
           const int slot = int(q % kTcStages);
           const uint32_t ph = (q / kTcStages) & 1u;
+          unsigned long long t0 = tr ? clock64() : 0;
           tc::wait(&a_full[slot], ph);
+          unsigned long long t1 = tr ? clock64() : 0;
           tc::wait(&b_full[slot], ph);
+          if (tr) {
+            wa += t1 - t0;
+            wb += clock64() - t1;
+          }
           tc::fence_after_sync();
-          for (int s = 0; s < p.ns; ++s) {
+          for (int s = 0; s < p.ns && !(p.ablate & 2); ++s) {
             const uint64_t bh = tc::desc_k_interleave(stage_b(slot, s, 0), 128, 256);
             const uint64_t bl = tc::desc_k_interleave(stage_b(slot, s, 1), 128, 256);
             for (int m = 0; m < p.mt; ++m) {
@@ -192,6 +204,11 @@ static __global__ void __launch_bounds__(320, 1)
           first = false;
         }
         tc::commit(&acc_full[tb]);
+        if (tr) {
+          tr[4] = wa;
+          tr[5] = wb;
+          tr[7] = clock64();
+        }
       }
     }
   } else if (warp < 4) {
@@ -234,10 +251,14 @@ static __global__ void __launch_bounds__(320, 1)
     for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
       int64_t j0, j1, itgt, split;
       unit_range(u, j0, j1, itgt, split);
-      gather(j0 + k, j1, itgt);
+      if (!(p.ablate & 1)) gather(j0 + k, j1, itgt);
       for (int64_t jb = j0; jb < j1; jb += kTcRows, ++q) {
         const int slot = int(q % kTcStages);
         tc::wait(&empty[slot], ((q / kTcStages) & 1u) ^ 1u);
+        if (p.ablate & 1) {
+          tc::arrive(&b_full[slot]);
+          continue;
+        }
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           if (s >= p.ns) break;
@@ -265,6 +286,26 @@ static __global__ void __launch_bounds__(320, 1)
     // ================= epilogue (warps 4..7: TMEM lane quarter = warp % 4) =================
     const int quarter = warp & 3;
     const int et = tid - 128;  // 0..127
+    // case B: out(r) = sum_k F_last(k, r) G(k, r) over this thread's k = m*128 +
+    // 32*quarter + lane, in steps (stream s, column chunk c, m-tile m).  The
+    // F_last values of a step do not depend on the accumulator, so they are
+    // loaded one step ahead (16-byte loads of the padded [K][N] fp32 copy) and
+    // the L2 round trip overlaps the previous step's TMEM read + FMAs.
+    constexpr int CW = N < 32 ? N : 32;
+    constexpr int NC = N / CW;
+    constexpr int V4 = CW / 4;
+    const int nsteps = p.ns * NC * p.mt;
+    float4 cur[V4], nxt[V4];
+    auto load_lf = [&](int step, float4(&dst)[V4]) {
+      const int m = step % p.mt;
+      const int c = (step / p.mt) % NC;
+      const int s = step / (p.mt * NC);
+      const int64_t k = int64_t(m) * 128 + quarter * 32 + lane;
+      const float4* src = reinterpret_cast<const float4*>((s ? p.lastfac[1] : p.lastfac[0]) + k * N + c * CW);
+#pragma unroll
+      for (int j = 0; j < V4; ++j) dst[j] = __ldg(src + j);
+    };
+    if (!p.caseA) load_lf(0, cur);
     uint32_t it = 0;
     for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++it) {
       int64_t j0, j1, itgt, split;
@@ -273,16 +314,18 @@ static __global__ void __launch_bounds__(320, 1)
       const uint32_t use = p.dbuf ? (it >> 1) : it;
       tc::wait(&acc_full[tb], use & 1u);
       tc::fence_after_sync();
-      for (int s = 0; s < p.ns; ++s) {
-        const uint32_t tcol = tmem + (uint32_t(quarter * 32) << 16) + tb * uint32_t(cols_per_buf) +
-                              uint32_t(s * p.mt * N);
-        if (p.caseA) {
+      unsigned long long* tr = (p.trace && it < 16 && et == 0) ? p.trace + (size_t(blockIdx.x) * 16 + it) * 8 : nullptr;
+      if (tr) tr[0] = clock64();
+      const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + tb * uint32_t(cols_per_buf);
+      if (p.ablate & 4) {
+      } else if (p.caseA) {
+        for (int s = 0; s < p.ns; ++s) {
           for (int m = 0; m < p.mt; ++m) {
             const int64_t k = int64_t(m) * 128 + quarter * 32 + lane;
 #pragma unroll
             for (int c0 = 0; c0 < N; c0 += 32) {
               uint32_t v[32];
-              tc::tmem_ld32(tcol + uint32_t(m * N + c0), v);
+              tc::tmem_ld32(tbase + uint32_t((s * p.mt + m) * N + c0), v);
               // one 128-byte row segment per thread, 16-byte stores (columns
               // R..RP-1 carry the zero B columns' G = 0)
               float4* dst = reinterpret_cast<float4*>(p.partA + ((int64_t(s) * p.units + u) * K + k) * p.RP + c0);
@@ -293,41 +336,44 @@ static __global__ void __launch_bounds__(320, 1)
                                            __uint_as_float(v[r + 2]), __uint_as_float(v[r + 3]));
             }
           }
-          continue;
         }
-        // case B: sum_k F_last(k, r) G(k, r) in fp64, 32 columns at a time
-        // (per column the k order is m ascending, as before)
+      } else {
+        float acc[CW];
+        for (int step = 0; step < nsteps; ++step) {
+          const int m = step % p.mt;
+          const int c = (step / p.mt) % NC;
+          const int s = step / (p.mt * NC);
+          load_lf(step + 1 < nsteps ? step + 1 : 0, nxt);  // next step, or the next unit's first
+          if (m == 0) {
 #pragma unroll
-        for (int c0 = 0; c0 < N; c0 += 32) {
-          constexpr int CW = N < 32 ? N : 32;
-          double acc[CW];
+            for (int r = 0; r < CW; ++r) acc[r] = 0.f;
+          }
+          uint32_t v[32];
+          tc::tmem_ld32(tbase + uint32_t((s * p.mt + m) * N + c * CW), v);
+          const float* f = reinterpret_cast<const float*>(cur);
+          // fp32 over the <= 4 m-tiles of one k residue (G is an fp32 MMA
+          // result; the cross-k and cross-unit sums below are fp64)
 #pragma unroll
-          for (int r = 0; r < CW; ++r) acc[r] = 0.0;
-          for (int m = 0; m < p.mt; ++m) {
-            const int64_t k = int64_t(m) * 128 + quarter * 32 + lane;
-            // the last-factor values do not depend on the accumulator: all
-            // loads in flight before the TMEM read (a load->DFMA chain per
-            // column serialises on L2 latency)
-            float lf[CW];
+          for (int r = 0; r < CW; ++r) acc[r] = fmaf(__uint_as_float(v[r]), f[r], acc[r]);
+          if (m == p.mt - 1) {
 #pragma unroll
-            for (int r = 0; r < CW; ++r) lf[r] = c0 + r < p.R ? __ldg(p.lastfac[s] + (c0 + r) * K + k) : 0.f;
-            uint32_t v[32];
-            tc::tmem_ld32(tcol + uint32_t(m * N + c0), v);
-#pragma unroll
-            for (int r = 0; r < CW; ++r) acc[r] = fma(double(__uint_as_float(v[r])), double(lf[r]), acc[r]);
+            for (int r = 0; r < CW; ++r) {
+              const double w = warp_sum(double(acc[r]));
+              if (lane == 0) red[quarter][c * CW + r] = w;
+            }
+            if (c == NC - 1) {
+              named_sync(1, 128);
+              if (et < p.R)
+                p.partB[((int64_t(s) * In + itgt) * p.S + split) * p.RP + et] =
+                    red[0][et] + red[1][et] + red[2][et] + red[3][et];
+              named_sync(1, 128);
+            }
           }
 #pragma unroll
-          for (int r = 0; r < CW; ++r) {
-            const double w = warp_sum(acc[r]);
-            if (lane == 0) red[quarter][c0 + r] = w;
-          }
+          for (int j = 0; j < V4; ++j) cur[j] = nxt[j];
         }
-        named_sync(1, 128);
-        if (et < p.R)
-          p.partB[((int64_t(s) * In + itgt) * p.S + split) * p.RP + et] =
-              red[0][et] + red[1][et] + red[2][et] + red[3][et];
-        named_sync(1, 128);
       }
+      if (tr) tr[1] = clock64();
       tc::fence_before_sync();
       tc::arrive(&acc_empty[tb]);
     }
@@ -337,13 +383,13 @@ static __global__ void __launch_bounds__(320, 1)
   if (warp == 9) tc::tmem_dealloc(tmem, uint32_t(p.tmem_cols));
 }
 
-// [K][R] fp64 -> [R][K] fp32, for the coalesced case-B epilogue reads
-static __global__ void transpose_kr_kernel(const double* src, int64_t K, int R, float* dst) {
+// [K][R] fp64 -> [K][N] fp32 zero padded, for the case-B epilogue's 16-byte loads
+static __global__ void pad_last_kernel(const double* src, int64_t K, int R, int N, float* dst) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i >= K * R) return;
-  const int64_t k = i % K;
-  const int r = int(i / K);
-  dst[i] = float(src[k * R + r]);
+  if (i >= K * N) return;
+  const int64_t k = i / N;
+  const int r = int(i % N);
+  dst[i] = r < R ? float(src[k * R + r]) : 0.f;
 }
 
 // host P~/Q~ (fp64) -> bf16 hi/lo planes (step-level uploads).  The split is

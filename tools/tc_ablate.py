@@ -1,0 +1,37 @@
+"""Role ablation of the tensor-core contraction on the C2 workload: per-launch
+contract time with B producers / MMAs / epilogue work switched off
+(NTFG_TC_ABLATE bits, set per subprocess).  Timing only -- results are wrong.
+usage: python tools/tc_ablate.py [beta]"""
+import json
+import os
+import subprocess
+import sys
+
+if len(sys.argv) > 2:  # child
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import bench
+    import paper_2602_14683_b200 as ntf
+    beta = float(sys.argv[1])
+    x, init = bench.make_problem(bench.DIMS, bench.RANK, 0, 0, bench.DIMS[0], torch.device("cuda", 0))
+    cfg = ntf.FitConfig(beta=beta, rank=bench.RANK, inner_steps=bench.INNER, max_iters=3, precision="f32",
+                        use_graphs=False)
+    ctx = ntf.default_context()
+    ctx.set_profiling(True)
+    try:
+        ntf.jcomm_fit(x, init, cfg)
+    except Exception as e:  # ablated runs can trip the domain checks
+        print("#", type(e).__name__, str(e)[:80], file=sys.stderr)
+    print(json.dumps(ctx.stats()))
+else:
+    beta = sys.argv[1] if len(sys.argv) > 1 else "0.5"
+    for bits in [0, 1, 2, 4, 5, 6, 7, 3]:
+        env = dict(os.environ, NTFG_TC_ABLATE=str(bits))
+        out = subprocess.run([sys.executable, __file__, beta, "child"], env=env, capture_output=True, text=True)
+        line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-300:]
+        try:
+            st = json.loads(line)
+            print(bits, "contract_ms/launch %.4f" % (st["contract_ms"] / max(st["contract_launches"], 1)),
+                  "recon_ms", round(st["recon_ms"], 3))
+        except Exception:
+            print(bits, line)
