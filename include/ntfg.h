@@ -133,6 +133,17 @@ ntfg_status ntfg_cp_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t a
                         int32_t x_location, const ntfg_shard* shard, double* factors_inout,
                         ntfg_trace_row* trace, uint64_t* trace_len);
 
+/* Sparse COO CP fit at beta = 1 (new; the reference densifies COO input in
+ * read_coo, io.cpp:87-142, and runs bcomm_fit / jcomm_fit, cp.hpp:48,76).
+ * indices: [nnz][order] int32 row-major, 0-based; values: nnz fp32/fp64;
+ * duplicates accumulate in input order (io.cpp:138).  Same results as the
+ * dense fit of the densified tensor up to summation order. */
+ntfg_status ntfg_cp_fit_coo(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t algo,
+                            uint32_t order, const uint64_t* dims, uint64_t nnz,
+                            const int32_t* indices, const void* values, int32_t values_dtype,
+                            int32_t location, double* factors_inout, ntfg_trace_row* trace,
+                            uint64_t* trace_len);
+
 /* tucker_bcomm_fit / tucker_jcomm_fit (reference tucker.hpp:55,84; tucker.cpp:221-275) */
 ntfg_status ntfg_tucker_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t algo,
                             uint32_t order, const uint64_t* dims, const void* x, int32_t x_dtype,

@@ -80,6 +80,8 @@ _SIGS = {
     "ntfg_validate_fit_config": [C.POINTER(FitConfigC)],
     "ntfg_cp_fit": [_V, C.POINTER(FitConfigC), C.c_int32, C.c_uint32, _U, _V, C.c_int32, C.c_int32,
                     C.POINTER(ShardC), _P, C.POINTER(TraceRowC), _U],
+    "ntfg_cp_fit_coo": [_V, C.POINTER(FitConfigC), C.c_int32, C.c_uint32, _U, C.c_uint64, _V, _V, C.c_int32,
+                        C.c_int32, _P, C.POINTER(TraceRowC), _U],
     "ntfg_tucker_fit": [_V, C.POINTER(FitConfigC), C.c_int32, C.c_uint32, _U, _V, C.c_int32, C.c_int32,
                         C.POINTER(ShardC), _P, _P, C.POINTER(TraceRowC), _U],
     "ntfg_cp_reconstruct": [_V, C.c_int32, C.c_uint32, _U, C.c_uint64, _P, _P],

@@ -270,6 +270,14 @@ def _split(flat: np.ndarray, shapes) -> List[np.ndarray]:
     return out
 
 
+def _is_cuda_tensor(x) -> bool:
+    try:
+        import torch
+        return isinstance(x, torch.Tensor) and x.is_cuda
+    except ImportError:
+        return False
+
+
 def _x_arg(x):
     """(dims, pointer, dtype code, location, keepalive) for host or device X."""
     try:
@@ -346,6 +354,55 @@ def bcomm_fit(x, init, cfg: FitConfig, ctx: Optional[Context] = None, shard=None
 def jcomm_fit(x, init, cfg: FitConfig, ctx: Optional[Context] = None, shard=None) -> CpFitResult:
     """Joint-MM CP fit (reference cp.cpp:271-298)."""
     return _cp_fit(1, x, init, cfg, ctx, shard)
+
+
+def _cp_fit_coo(algo: int, indices, values, dims, init, cfg: FitConfig, ctx=None) -> CpFitResult:
+    ctx = ctx or default_context()
+    dims = [int(d) for d in dims]
+    init = [_f64(a) for a in init]
+    cfgc, keep_r = cfg._c()
+    _check(N.load().ntfg_validate_fit_config(C.byref(cfgc)))
+    r = _check_cp_model(init, dims, "coo fit")
+    if r != cfg.rank:
+        cfgc.rank = r
+    keep = []
+    if _is_cuda_tensor(indices):
+        import torch
+        idx = indices.to(torch.int32).contiguous()
+        val = values.contiguous()
+        if idx.dim() != 2 or idx.shape[1] != len(dims) or val.numel() != idx.shape[0]:
+            raise ShapeError("coo fit: indices must be [nnz, order] with one value per nonzero")
+        keep += [idx, val]
+        ip, vp, vdt, loc, nnz = C.c_void_p(idx.data_ptr()), C.c_void_p(val.data_ptr()), \
+            (1 if val.dtype == torch.float32 else 0), 1, idx.shape[0]
+        if val.dtype not in (torch.float32, torch.float64):
+            raise ShapeError("coo fit: values must be float32 or float64")
+    else:
+        idx = np.ascontiguousarray(np.asarray(indices), dtype=np.int32)
+        val = np.asarray(values)
+        val = np.ascontiguousarray(val, dtype=np.float32 if val.dtype == np.float32 else np.float64)
+        if idx.ndim != 2 or idx.shape[1] != len(dims) or val.size != idx.shape[0]:
+            raise ShapeError("coo fit: indices must be [nnz, order] with one value per nonzero")
+        keep += [idx, val]
+        ip, vp, vdt, loc, nnz = C.c_void_p(idx.ctypes.data), C.c_void_p(val.ctypes.data), \
+            (1 if val.dtype == np.float32 else 0), 0, idx.shape[0]
+    f = _cat(init)
+    rows = (N.TraceRowC * (int(cfg.max_iters) + 1))()
+    n = C.c_uint64(0)
+    _check(N.load().ntfg_cp_fit_coo(ctx.h, C.byref(cfgc), algo, len(dims), _u64(dims).ctypes.data_as(_UP),
+                                    int(nnz), ip, vp, vdt, loc, _dp(f), rows, C.byref(n)))
+    return CpFitResult(_split(f, [a.shape for a in init]), _trace(rows, n.value))
+
+
+def bcomm_fit_coo(indices, values, dims, init, cfg: FitConfig, ctx: Optional[Context] = None) -> CpFitResult:
+    """Block-MM CP fit of a sparse COO count tensor at beta = 1 (new; the
+    reference densifies COO input, io.cpp:87-142, then runs bcomm_fit)."""
+    return _cp_fit_coo(0, indices, values, dims, init, cfg, ctx)
+
+
+def jcomm_fit_coo(indices, values, dims, init, cfg: FitConfig, ctx: Optional[Context] = None) -> CpFitResult:
+    """Joint-MM CP fit of a sparse COO count tensor at beta = 1 (see bcomm_fit_coo)."""
+    return _cp_fit_coo(1, indices, values, dims, init, cfg, ctx)
 
 
 # ---------------------------------------------------------------------------

@@ -10,6 +10,8 @@ namespace ntfg {
 // cp_api.cu
 void cp_fit(Context&, const ntfg_fit_config&, int, uint32_t, const uint64_t*, const void*, int, int,
             const ntfg_shard*, double*, ntfg_trace_row*, uint64_t*);
+void cp_fit_coo(Context&, const ntfg_fit_config&, int, uint32_t, const uint64_t*, uint64_t, const int32_t*,
+                const void*, int, int, double*, ntfg_trace_row*, uint64_t*);
 void cp_reconstruct(Context&, int, uint32_t, const uint64_t*, uint64_t, const double*, double*);
 void cp_contract(Context&, int, uint32_t, const uint64_t*, const double*, uint64_t, const double*,
                  uint32_t, double*);
@@ -178,6 +180,20 @@ NTFG_API ntfg_status ntfg_cp_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, 
     need(cfg, "cfg"); need(dims, "dims"); need(x, "x"); need(factors, "factors");
     need(trace, "trace"); need(trace_len, "trace_len");
     ntfg::cp_fit(c, *cfg, algo, order, dims, x, x_dtype, x_location, shard, factors, trace, trace_len);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_fit_coo(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t algo,
+                                     uint32_t order, const uint64_t* dims, uint64_t nnz,
+                                     const int32_t* indices, const void* values, int32_t values_dtype,
+                                     int32_t location, double* factors, ntfg_trace_row* trace,
+                                     uint64_t* trace_len) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(cfg, "cfg"); need(dims, "dims"); need(factors, "factors");
+    need(trace, "trace"); need(trace_len, "trace_len");
+    if (nnz > 0) { need(indices, "indices"); need(values, "values"); }
+    ntfg::cp_fit_coo(c, *cfg, algo, order, dims, nnz, indices, values, values_dtype, location, factors, trace,
+                     trace_len);
   });
 }
 

@@ -2,6 +2,7 @@
 // Reference: include/ntf/cp.hpp, src/cp.cpp; see include/ntfg.h for the
 // per-function mapping.
 #include <cmath>
+#include <functional>
 #include <vector>
 
 #include "cp_engine.cuh"
@@ -31,12 +32,12 @@ std::vector<double> nesterov_alphas(uint64_t K) {
 
 template <typename T>
 std::vector<ntfg_trace_row> cp_fit_t(Context& c, const ntfg_fit_config& cfg, int algo,
-                                     uint32_t order, const uint64_t* dims, const void* x,
-                                     int dtype, int loc, const ntfg_shard* shard,
-                                     double* factors) {
+                                     uint32_t order, const uint64_t* dims,
+                                     const std::function<void(CpEngine<T>&)>& set_data,
+                                     const ntfg_shard* shard, double* factors) {
   CpEngine<T> e(c, order, dims, int64_t(cfg.rank), cfg.beta, cfg.eps, shard);
   if (algo == NTFG_JCOMM) check_positive_host(factors, e.factor_doubles(), "chi1");
-  e.set_x(x, dtype, loc);
+  set_data(e);
   e.set_factors_host(factors);
   e.prealloc(cfg.beta == 1.0 ? 1 : 2);
   double* losses = c.buf<double>("fit.losses", cfg.max_iters + 2);
@@ -113,8 +114,26 @@ void cp_fit(Context& c, const ntfg_fit_config& cfg, int algo, uint32_t order, co
   c.stats = ntfg_stats{};
   std::vector<ntfg_trace_row> tr =
       cfg.precision == NTFG_F32
-          ? cp_fit_t<float>(c, cfg, algo, order, dims, x, dtype, loc, shard, factors)
-          : cp_fit_t<double>(c, cfg, algo, order, dims, x, dtype, loc, shard, factors);
+          ? cp_fit_t<float>(c, cfg, algo, order, dims, [&](CpEngine<float>& e) { e.set_x(x, dtype, loc); },
+                            shard, factors)
+          : cp_fit_t<double>(c, cfg, algo, order, dims, [&](CpEngine<double>& e) { e.set_x(x, dtype, loc); },
+                             shard, factors);
+  for (size_t i = 0; i < tr.size(); ++i) trace[i] = tr[i];
+  *trace_len = tr.size();
+}
+
+// sparse COO fit at beta = 1 (K7, coo_kernels.cuh): all passes in fp64
+// whatever cfg.precision says (the nonzero pass is latency-bound, not
+// bandwidth-bound, so fp32 storage buys nothing).
+void cp_fit_coo(Context& c, const ntfg_fit_config& cfg, int algo, uint32_t order, const uint64_t* dims,
+                uint64_t nnz, const int32_t* indices, const void* values, int dtype, int loc, double* factors,
+                ntfg_trace_row* trace, uint64_t* trace_len) {
+  validate_config(cfg);
+  if (algo != NTFG_BCOMM && algo != NTFG_JCOMM) throw Error(NTFG_ERR_DOMAIN, "unknown algorithm");
+  c.stats = ntfg_stats{};
+  std::vector<ntfg_trace_row> tr = cp_fit_t<double>(
+      c, cfg, algo, order, dims,
+      [&](CpEngine<double>& e) { e.set_coo(nnz, indices, values, dtype, loc); }, nullptr, factors);
   for (size_t i = 0; i < tr.size(); ++i) trace[i] = tr[i];
   *trace_len = tr.size();
 }

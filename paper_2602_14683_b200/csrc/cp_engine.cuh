@@ -12,8 +12,10 @@
 #include <cstdlib>
 #include <mutex>
 #include <set>
+#include <string>
 #include <vector>
 
+#include "coo_kernels.cuh"
 #include "cp_kernels.cuh"
 #include "engine.cuh"
 #include "stream3_kernels.cuh"
@@ -438,6 +440,10 @@ class CpEngine {
 
   // Allocate every buffer a fit can touch (no cudaMalloc during graph capture).
   void prealloc(int ns) {
+    if (sparse_) {
+      if (!n1num_) n1num_ = c_.buf<double>("cp.n1num", factor_doubles() + size_t(max_dim()) * R_);
+      return;
+    }
     size_t a = 0, b = 0;
     for (int n = 0; n < N_; ++n) {
       for (int v = 0; v < 2; ++v) {
@@ -568,6 +574,14 @@ class CpEngine {
   void block_update(int n, const double* anchor, bool objective) {
     const double* fac[kMaxOrder];
     for (int m = 0; m < N_; ++m) fac[m] = (m == n) ? anchor : A(m);
+    if (sparse_) {
+      if (objective && n != 0) coo_objective(fac);
+      coo_num(n, fac, numden_, objective && n == 0);
+      if (objective && n == 0) coo_finish_objective(fac);
+      colprod(fac, n);
+      coo_finalize(n, numden_, anchor, nullptr);
+      return;
+    }
     const T* alast = stage_;
     if (n == N_ - 1 && anchor != A(n)) {
       stage(anchor, stage_anchor_);
@@ -605,6 +619,10 @@ class CpEngine {
     c_.d2d(chi2_, A_, bytes);
     const double* fac[kMaxOrder];
     for (int m = 0; m < N_; ++m) fac[m] = A(m);
+    if (sparse_) {  // the objective rides on the mode-0 numerator pass (n1_numerators)
+      coo_pending_obj_ = objective;
+      return;
+    }
     recon_pq(fac, stage_, beta_ != 1.0, objective);
   }
 
@@ -636,6 +654,16 @@ class CpEngine {
   // by all L sweeps; the denominator is the closed form of cp.cpp:224-225.
   void n1_numerators() {
     if (!n1num_) n1num_ = c_.buf<double>("cp.n1num", factor_doubles() + size_t(max_dim()) * R_);
+    if (sparse_) {
+      const double* fac[kMaxOrder];
+      for (int m = 0; m < N_; ++m) fac[m] = Aref_ + off_[m];
+      for (int n = 0; n < N_; ++n) {
+        coo_num(n, fac, n1num_ + off_[n], n == 0 && coo_pending_obj_);
+        if (n == 0 && coo_pending_obj_) coo_finish_objective(fac);
+      }
+      coo_pending_obj_ = false;
+      return;
+    }
     Stream st[2];
     st[0].src = p_;
     st[1].src = p_;
@@ -677,7 +705,7 @@ class CpEngine {
   // jcomm_outer_step (cp.cpp:231-240)
   void jcomm_outer(int inner_steps, bool fuse_objective) {
     jcomm_reference(fuse_objective);
-    if (beta_ == 1.0 && n1_enabled_) {
+    if (beta_ == 1.0 && (n1_enabled_ || sparse_)) {
       n1_numerators();
       for (int l = 0; l < inner_steps; ++l)
         for (int n = 0; n < N_; ++n) jcomm_inner_n1(n);
@@ -699,8 +727,201 @@ class CpEngine {
   void objective() {
     const double* fac[kMaxOrder];
     for (int m = 0; m < N_; ++m) fac[m] = A(m);
+    if (sparse_) {
+      coo_objective(fac);
+      return;
+    }
     recon(fac, stage_, nullptr, nullptr, true);
   }
+
+  // ---- sparse COO data (K7, coo_kernels.cuh; beta = 1 only) -------------------------------
+  // indices: [nnz][order] int32 row-major (host or device), values fp32/fp64.
+  // Duplicates are summed in input order (as read_coo's dense +=, io.cpp:138);
+  // one copy of the merged nonzeros per mode, stably sorted by that mode's index.
+  void set_coo(uint64_t nnz, const int32_t* indices, const void* values, int dtype, int location) {
+    if (beta_ != 1.0) throw Error(NTFG_ERR_DOMAIN, "sparse COO fits require beta = 1");
+    if (R_ > 64) throw Error(NTFG_ERR_SHAPE, "sparse COO fits support rank <= 64");
+    if (sharded_) throw Error(NTFG_ERR_SHAPE, "sparse COO fits are single-device");
+    const size_t N = size_t(N_);
+    std::vector<int32_t> hidx(size_t(nnz) * N);
+    std::vector<double> hval(nnz);
+    if (location == NTFG_DEVICE) {
+      c_.d2h(hidx.data(), indices, hidx.size() * sizeof(int32_t));
+      if (dtype == 1) {
+        std::vector<float> f(nnz);
+        c_.d2h(f.data(), values, nnz * sizeof(float));
+        c_.sync();
+        for (size_t j = 0; j < nnz; ++j) hval[j] = f[j];
+      } else {
+        c_.d2h(hval.data(), values, nnz * sizeof(double));
+      }
+      c_.sync();
+    } else {
+      std::copy(indices, indices + hidx.size(), hidx.begin());
+      for (size_t j = 0; j < nnz; ++j)
+        hval[j] = dtype == 1 ? double(static_cast<const float*>(values)[j]) : static_cast<const double*>(values)[j];
+    }
+    // linear keys (row-major) + stable order -> merged, lexicographically sorted nonzeros
+    std::vector<int64_t> key(nnz);
+    for (size_t j = 0; j < nnz; ++j) {
+      int64_t k = 0;
+      for (size_t m = 0; m < N; ++m) {
+        const int32_t i = hidx[j * N + m];
+        if (i < 0 || int64_t(i) >= g_.dims[m]) throw Error(NTFG_ERR_SHAPE, "COO index out of range");
+        k = k * g_.dims[m] + i;
+      }
+      key[j] = k;
+    }
+    std::vector<int64_t> ord(nnz);
+    for (size_t j = 0; j < nnz; ++j) ord[j] = int64_t(j);
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+    std::vector<int32_t> midx;
+    std::vector<double> mval;
+    midx.reserve(hidx.size());
+    mval.reserve(nnz);
+    for (size_t t = 0; t < nnz;) {
+      const int64_t k = key[ord[t]];
+      double v = 0.0;
+      const size_t first = size_t(ord[t]);
+      for (; t < nnz && key[ord[t]] == k; ++t) v += hval[ord[t]];
+      for (size_t m = 0; m < N; ++m) midx.push_back(hidx[first * N + m]);
+      mval.push_back(v);
+    }
+    const size_t M = mval.size();
+    coo_nnz_ = int64_t(M);
+    coo_.assign(N, CooMode{});
+    size_t max_pieces = 1;
+    for (int n = 0; n < N_; ++n) {
+      // stable counting sort by i_n
+      const int64_t In = g_.dims[n];
+      std::vector<int64_t> cnt(size_t(In) + 1, 0);
+      for (size_t j = 0; j < M; ++j) ++cnt[size_t(midx[j * N + n]) + 1];
+      for (int64_t i = 0; i < In; ++i) cnt[size_t(i) + 1] += cnt[size_t(i)];
+      std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1), perm(M);
+      for (size_t j = 0; j < M; ++j) perm[size_t(pos[size_t(midx[j * N + n])]++)] = int64_t(j);
+      // pieces of <= kCooPiece nonzeros inside one key
+      std::vector<int64_t> pstart, kpiece(size_t(In) + 1);
+      for (int64_t i = 0; i < In; ++i) {
+        kpiece[size_t(i)] = int64_t(pstart.size());
+        for (int64_t b = cnt[size_t(i)]; b < cnt[size_t(i) + 1]; b += kCooPiece) pstart.push_back(b);
+      }
+      kpiece[size_t(In)] = int64_t(pstart.size());
+      const int64_t np = int64_t(pstart.size());
+      pstart.push_back(int64_t(M));
+      CooMode& cm = coo_[size_t(n)];
+      cm.npieces = np;
+      max_pieces = std::max(max_pieces, size_t(np));
+      const std::string tag = "coo." + std::to_string(n) + ".";
+      std::vector<int32_t> col(M);
+      for (size_t m = 0; m < N; ++m) {
+        for (size_t j = 0; j < M; ++j) col[j] = midx[size_t(perm[j]) * N + m];
+        cm.idx[m] = c_.buf<int32_t>(tag + "idx" + std::to_string(m), std::max<size_t>(M, 1));
+        c_.h2d(cm.idx[m], col.data(), M * sizeof(int32_t));
+        c_.sync();
+      }
+      std::vector<double> v(M);
+      for (size_t j = 0; j < M; ++j) v[j] = mval[size_t(perm[j])];
+      cm.val = c_.buf<double>(tag + "val", std::max<size_t>(M, 1));
+      c_.h2d(cm.val, v.data(), M * sizeof(double));
+      cm.piece_start = c_.buf<int64_t>(tag + "pstart", pstart.size());
+      c_.h2d(cm.piece_start, pstart.data(), pstart.size() * sizeof(int64_t));
+      cm.key_piece = c_.buf<int64_t>(tag + "kpiece", kpiece.size());
+      c_.h2d(cm.key_piece, kpiece.data(), kpiece.size() * sizeof(int64_t));
+      c_.sync();
+    }
+    coo_partial_ = c_.buf<double>("coo.partial", max_pieces * size_t(R_));
+    coo_obj_ = c_.buf<double>("coo.obj", max_pieces);
+    coo_closed_ = c_.buf<double>("coo.closed", 1);
+    sparse_ = true;
+    tc_ = false;
+  }
+  int64_t coo_nnz() const { return coo_nnz_; }
+
+ private:
+  struct CooMode {
+    int32_t* idx[kMaxOrder] = {};
+    double* val = nullptr;
+    int64_t* piece_start = nullptr;
+    int64_t* key_piece = nullptr;
+    int64_t npieces = 0;
+  };
+
+  // Num^(n) of the model `fac` into out[I_n][R]; with objective, the nnz part of
+  // D_1 per mode-0 piece into coo_obj_ (n must be 0)
+  void coo_num(int n, const double* const* fac, double* out, bool objective) {
+    launch_coo_pieces(n, fac, true, objective);
+    const int64_t In = g_.dims[n];
+    const int grid = int(std::min<int64_t>(In, int64_t(c_.sm_count) * 8));
+    coo_key_reduce_kernel<<<grid, 256, 0, c_.stream>>>(coo_partial_, coo_[size_t(n)].key_piece, In, int(R_), out);
+    NTFG_LAUNCHED(c_);
+  }
+  void launch_coo_pieces(int n, const double* const* fac, bool partials, bool objective) {
+    const CooMode& cm = coo_[size_t(n)];
+    CooPieceParams pp{};
+    pp.order = N_;
+    pp.n = n;
+    pp.R = int(R_);
+    for (int m = 0; m < N_; ++m) {
+      pp.idx[m] = cm.idx[m];
+      pp.fac[m] = fac[m];
+    }
+    pp.val = cm.val;
+    pp.piece_start = cm.piece_start;
+    pp.npieces = cm.npieces;
+    pp.eps = eps_;
+    pp.partial = partials ? coo_partial_ : nullptr;
+    pp.obj = objective ? coo_obj_ : nullptr;
+    pp.flags = flags_;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(cm.npieces, 8), int64_t(c_.sm_count) * 16)));
+    const int ph = c_.prof_begin(1);
+    if (R_ <= 32) coo_piece_kernel<1><<<grid, 256, 0, c_.stream>>>(pp);
+    else coo_piece_kernel<2><<<grid, 256, 0, c_.stream>>>(pp);
+    NTFG_LAUNCHED(c_);
+    c_.prof_end(ph);
+  }
+  // D_1 = [nnz part] + sum_r prod_m colsum(A_m)(r), mean over all entries
+  void coo_finish_objective(const double* const* fac) {
+    colprod(fac, -1);
+    closed_sum_kernel<<<1, 32, 0, c_.stream>>>(colprod_, int(R_), coo_closed_);
+    NTFG_LAUNCHED(c_);
+    objective_finalize_kernel<<<1, 256, 0, c_.stream>>>(coo_obj_, int(coo_[0].npieces), 1.0 / double(E_global_),
+                                                       losses_, counter_, nullptr, coo_closed_);
+    NTFG_LAUNCHED(c_);
+  }
+  void coo_objective(const double* const* fac) {
+    launch_coo_pieces(0, fac, false, true);
+    coo_finish_objective(fac);
+  }
+  // MU step of mode n from Num (numden layout, den closed form in colprod_)
+  void coo_finalize(int n, double* num, const double* anchor, const double* ref) {
+    FinalizeParams<T> f{};
+    f.In = g_.dims[n];
+    f.R = int(R_);
+    f.RP = RP_;
+    f.den_closed = 1;
+    f.colprod = colprod_;
+    f.phase = 2;
+    f.numden = num;
+    f.anchor = anchor;
+    f.out = A(n);
+    f.ref = ref;
+    f.stage = n == N_ - 1 ? stage_ : nullptr;
+    f.gamma = gamma_;
+    f.eps = eps_;
+    f.beta = beta_;
+    f.flags = flags_;
+    finalize_kernel<T><<<int(ceil_div(g_.dims[n] * RP_, 256)), 256, 0, c_.stream>>>(f);
+    NTFG_LAUNCHED(c_);
+  }
+  std::vector<CooMode> coo_;
+  bool sparse_ = false;
+  bool coo_pending_obj_ = false;
+  int64_t coo_nnz_ = 0;
+  double* coo_partial_ = nullptr;
+  double* coo_obj_ = nullptr;
+  double* coo_closed_ = nullptr;
+
+ public:
 
   double* Aref_all() const { return Aref_; }
   double* anchors() const { return anch_; }

@@ -357,20 +357,28 @@ struct TailConst {
   float e, b, b1, b2, ib;  // eps, beta, beta-1, beta-2, 1/(beta(beta-1))
 };
 
+// c >= eps > 0 here; the .ftz approximation skips the denormal scaling
+// rsqrtf() carries (an fp32 eps below FLT_MIN is not representable anyway)
+__device__ __forceinline__ float rsqrt_ftz(float c) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(c));
+  return r;
+}
+
 template <int BK>
 __device__ __forceinline__ void tc_weights(float x, float y, const TailConst& k, float& pv, float& qv,
                                            bool obj, float& oacc, unsigned& bad) {
   const float c = y < k.e ? k.e : y;  // std::max(xhat, eps)
-  // identical formulas to weights_entry(float, ...)
+  // same formulas as weights_entry(float, ...) (identical results for normal c)
   if constexpr (BK == kBeta1) {
     pv = __fdividef(x, c);
     qv = 1.f;
   } else if constexpr (BK == kBetaHalf) {
-    const float rs = rsqrtf(c);
+    const float rs = rsqrt_ftz(c);
     qv = rs;
     pv = x * __fdividef(rs, c);
   } else if constexpr (BK == kBeta3Half) {
-    const float rs = rsqrtf(c);
+    const float rs = rsqrt_ftz(c);
     qv = c * rs;
     pv = x * rs;
   } else if constexpr (BK == kBeta0) {
@@ -544,6 +552,12 @@ static __global__ void __launch_bounds__(128) recon3_kernel(const ReconParams<T>
     tma::wait(&bars[i % kDepth], unsigned((i / kDepth) & 1));
     const int64_t row0 = (rb0 + i * rb_stride) * kRows;
     const T* xrow = ring + size_t(i % kDepth) * kRows * W + tid * KT;
+    // plane element offset of (row0, k0); rows advance by K (tensor-core flavour)
+    const int64_t off0 = row0 * K + k0;
+    __nv_bfloat16* const pl0 = static_cast<__nv_bfloat16*>(p.planes[0]) + off0;
+    __nv_bfloat16* const pl1 = static_cast<__nv_bfloat16*>(p.planes[1]) + off0;
+    __nv_bfloat16* const pl2 = static_cast<__nv_bfloat16*>(p.planes[2]) + off0;
+    __nv_bfloat16* const pl3 = static_cast<__nv_bfloat16*>(p.planes[3]) + off0;
 #pragma unroll
     for (int rr = 0; rr < kRows; ++rr) {
       const int64_t row = row0 + rr;
@@ -577,12 +591,9 @@ static __global__ void __launch_bounds__(128) recon3_kernel(const ReconParams<T>
         for (int kk = 0; kk < KT; ++kk)
           tc_weights<BK>(float(xv[kk]), float(xhp[kk]), tk, pw[kk], qw[kk], want_obj, oacc, bad);
         if (want_obj) obj += double(oacc);
-        const int64_t off = row * K + k0;
-        store_planes<KT>(pw, static_cast<__nv_bfloat16*>(p.planes[0]) + off,
-                         static_cast<__nv_bfloat16*>(p.planes[1]) + off);
-        if constexpr (BK != kBeta1)
-          store_planes<KT>(qw, static_cast<__nv_bfloat16*>(p.planes[2]) + off,
-                           static_cast<__nv_bfloat16*>(p.planes[3]) + off);
+        const int ro = rr * int(K);  // < 2^31: rows of one block
+        store_planes<KT>(pw, pl0 + ro, pl1 + ro);
+        if constexpr (BK != kBeta1) store_planes<KT>(qw, pl2 + ro, pl3 + ro);
         continue;
       }
       T pw[KT], qw[KT];

@@ -185,3 +185,18 @@ def test_oracle_vs_reference_step_level(beta):
         c, ff = R.tucker_step(kind, x, core, fs, beta=beta)
         oc, off = fn()
         assert O.rel_err(c, oc) < 1e-12 and relm(ff, off) < 1e-12
+
+
+def test_coo_densify_accumulates_duplicates_in_order():
+    # read_coo io.cpp:138: dense[idx] += v, line by line
+    idx = np.array([[0, 1], [1, 0], [0, 1], [0, 1]], dtype=np.int32)
+    vals = np.array([1.0, 2.0, 0.1, 0.2])
+    d = O.coo_densify(idx, vals, (2, 2))
+    assert d[0, 1] == (1.0 + 0.1) + 0.2 and d[1, 0] == 2.0 and d[0, 0] == 0.0
+
+
+def test_coo_synthetic_conventions():
+    idx, vals = O.coo_synthetic((10, 50), 5000, seed=0, zipf_modes=(1,))
+    assert idx.dtype == np.int32 and idx.min() >= 0 and idx[:, 1].max() < 50
+    assert vals.min() == 1.0  # failures-count geometric: support {1, 2, ...}
+    assert np.bincount(idx[:, 1]).argmax() == 0  # Zipf head at index 0
