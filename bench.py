@@ -220,7 +220,51 @@ def run_ours(args, rank_id, world, local_rank):
                        "(X upload + factor/trace download inside the timed region); value = K / wall time"}
         del xh
 
-    return per_beta, launches, pst, clocks, e2e
+    c4 = run_c4(args, ctx, dev) if world == 1 and args.c4 else None
+    return per_beta, launches, pst, clocks, e2e, c4
+
+
+C4_DIMS = (183, 24, 1140, 1717)
+C4_NNZ = 3_300_000
+C4_RANK = 20
+C4_INNER = 3
+
+
+def c4_problem(seed: int = 0):
+    """C4 stand-in: modes 0,1 uniform, modes 2,3 Zipf(1.1)
+    truncated to [0, I_n); values 1 + Geometric(0.5) counted as failures
+    ({1, 2, ...}); duplicates kept (they accumulate on ingestion)."""
+    rng = np.random.default_rng(seed)
+    cols = []
+    for m, d in enumerate(C4_DIMS):
+        if m >= 2:
+            w = 1.0 / np.arange(1, d + 1) ** 1.1
+            cols.append(rng.choice(d, size=C4_NNZ, p=w / w.sum()))
+        else:
+            cols.append(rng.integers(0, d, size=C4_NNZ))
+    idx = np.stack(cols, axis=1).astype(np.int32)
+    vals = (1 + (rng.geometric(0.5, size=C4_NNZ) - 1)).astype(np.float32)
+    init = [0.1 + rng.random((d, C4_RANK)) for d in C4_DIMS]
+    return idx, vals, init
+
+
+def run_c4(args, ctx, dev):
+    """C4: sparse COO CP, R=20, beta=1, J-CoMM L=3 (K7 path), COO resident on
+    the device; value = outer iterations / device time of the K timed steps."""
+    import torch
+    import paper_2602_14683_b200 as ntf
+    idx, vals, init = c4_problem(0)
+    di = torch.from_numpy(idx).to(dev)
+    dv = torch.from_numpy(vals).to(dev)
+    cfg = lambda it: ntf.FitConfig(beta=1.0, rank=C4_RANK, inner_steps=C4_INNER, max_iters=it, precision="f64")
+    ntf.jcomm_fit_coo(di, dv, C4_DIMS, init, cfg(args.warmup), ctx=ctx)
+    res = ntf.jcomm_fit_coo(di, dv, C4_DIMS, init, cfg(args.steps), ctx=ctx)
+    st = ctx.stats()
+    ms = st["device_ms"]
+    return {"workload": "C4: sparse COO CP 183x24x1140x1717, 3.3M nnz (Zipf modes 2,3), R=20, beta=1, "
+                        "J-CoMM L=3, fp64", "outer_it_per_s": args.steps / (ms * 1e-3),
+            "ms_per_step": ms / args.steps, "final_loss": res.trace[-1].loss,
+            "gpu_launches": st["kernel_launches"]}
 
 
 # ---------------------------------------------------------------------------
@@ -305,6 +349,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-c4", dest="c4", action="store_false", help="skip the sparse C4 side measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -322,7 +367,7 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
-    per_beta, launches, pst, clocks, e2e = run_ours(args, rank_id, world, local_rank)
+    per_beta, launches, pst, clocks, e2e, c4 = run_ours(args, rank_id, world, local_rank)
 
     if rank_id == 0:
         E = int(np.prod(DIMS))
@@ -341,7 +386,7 @@ def main():
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                cpu = cpu_sample(1)
+                cpu = cpu_sample(2)
             except Exception as ex:  # the baseline must never sink the bench line
                 cpu = {"value": None, "unit": "outer_it/s", "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
         line = {
@@ -353,12 +398,12 @@ def main():
                        "global_batch": 1, "seq_len": 0, "parallelism": f"mode-0 slabs dp{world}",
                        "l2": "inputs (X 0.5 GB, P~/Q~ 1 GB) exceed L2; no flush"},
             "per_beta": {str(b): v for b, v in per_beta.items()},
-            "roofline": {"bound": "hbm", "kernel": "contract_kernel (K3 J-CoMM inner pass)",
+            "roofline": {"bound": "hbm", "kernel": "tc_contract_kernel (K3 J-CoMM inner pass, tcgen05)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_source": peak_src, "traffic": traffic,
                          "algorithmic_bytes_per_launch": ebytes, "avg_launch_ms": avg_ms,
                          "fma_rate_tflops_equiv": fma_rate, "fma_frac": fma_rate / FFMA_PEAK_T},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "c4_sparse": c4,
             "kernel_breakdown_ms_per_step": {
                 "recon": pst["recon_ms"] / max(1, min(args.steps, 5)),
                 "contract": pst["contract_ms"] / max(1, min(args.steps, 5)),

@@ -144,6 +144,40 @@ ntfg_status ntfg_cp_fit_coo(ntfg_context* ctx, const ntfg_fit_config* cfg, int32
                             int32_t location, double* factors_inout, ntfg_trace_row* trace,
                             uint64_t* trace_len);
 
+/* ---- data ingestion and generation (reference io.hpp / io.cpp) ---------------
+ * ctx may be NULL for host-only calls (location NTFG_HOST). */
+
+/* CTF1 header (read_tensor io.cpp:46-77 checks): order and dims (capacity
+ * dims_capacity); max_entries = 0 disables the entry budget (kDefaultEntryBudget
+ * io.hpp:19 is 2^27). */
+ntfg_status ntfg_ctf1_header(const char* path, uint32_t* order, uint64_t* dims, uint32_t dims_capacity,
+                             uint64_t max_entries);
+/* CTF1 payload into dst (fp64 -> x_dtype), host or device; device reads stream
+ * through pinned staging without a full host copy. */
+ntfg_status ntfg_ctf1_read(ntfg_context* ctx, const char* path, void* dst, int32_t dtype, int32_t location,
+                           uint64_t max_entries);
+/* write_tensor (io.cpp:30-44): byte-exact CTF1 from a host or device tensor. */
+ntfg_status ntfg_ctf1_write(ntfg_context* ctx, const char* path, uint32_t order, const uint64_t* dims,
+                            const void* src, int32_t dtype, int32_t location);
+/* read_coo grammar (io.cpp:87-142) as nonzeros: indices == NULL counts only
+ * (nnz out); otherwise fills [nnz][order] int32 indices and fp64 values. */
+ntfg_status ntfg_coo_text_read(const char* path, uint32_t* order, uint64_t* dims, uint32_t dims_capacity,
+                               uint64_t* nnz, int32_t* indices, double* values, uint64_t capacity,
+                               uint64_t max_entries);
+/* write_trace (io.cpp:154-164): "iter,time_s,loss", %.17g. */
+ntfg_status ntfg_trace_write(const char* path, const ntfg_trace_row* rows, uint64_t n);
+/* Counter-based generator (new): Philox4x32-10 keyed by (seed, stream),
+ * uniform #j = (word >> 11) * 2^-53.  Streams: 1 truth factors, 2 init, 3 noise. */
+ntfg_status ntfg_philox_uniforms(uint64_t seed, uint64_t stream, uint64_t offset, uint64_t n, double* out);
+/* CP factors from the generator: which = 0 truth (U clamped to eps), 1 init (0.1 + U). */
+ntfg_status ntfg_cp_factors_generate(uint32_t order, const uint64_t* dims, uint64_t rank, uint64_t seed,
+                                     int32_t which, double eps, double* out);
+/* X = [[truth]] * Gamma(gamma_k, gamma_theta) for mode-0 rows [row0, row1),
+ * generated in place on the device (BASELINE C2/C5 data). */
+ntfg_status ntfg_generate_cp_gamma(ntfg_context* ctx, uint32_t order, const uint64_t* dims, uint64_t rank,
+                                   uint64_t seed, uint32_t gamma_k, double gamma_theta, uint64_t row0,
+                                   uint64_t row1, void* x_device, int32_t dtype);
+
 /* tucker_bcomm_fit / tucker_jcomm_fit (reference tucker.hpp:55,84; tucker.cpp:221-275) */
 ntfg_status ntfg_tucker_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t algo,
                             uint32_t order, const uint64_t* dims, const void* x, int32_t x_dtype,

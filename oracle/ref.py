@@ -234,3 +234,43 @@ def init_cp_factors(dims, rank, seed, eps=1e-12):
     _check(lib().ntfref_init_cp_factors(C.c_int(len(dims)), _u64(dims).ctypes.data_as(_U), C.c_int(rank),
                                         C.c_uint64(seed), C.c_double(eps), _d(out)))
     return _split(out, [(d, rank) for d in dims])
+
+
+# ---- I/O (reference io.cpp) ---------------------------------------------------
+
+def write_tensor(path: str, x: np.ndarray) -> None:
+    lib().ntfref_write_tensor.argtypes = [C.c_char_p, C.c_int, _U, _P]
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    dims = _u64(x.shape)
+    _check(lib().ntfref_write_tensor(path.encode(), x.ndim, dims.ctypes.data_as(_U), _d(x)))
+
+
+def read_coo_dense(path: str, cap: int, floor: Optional[float] = None) -> np.ndarray:
+    """read_coo through the shim, in a child interpreter that has not loaded
+    NumPy (the reference's iostream parsing crashes inside a NumPy process
+    here -- an environment quirk, not a reference behaviour)."""
+    import json
+    import subprocess
+    import sys
+    code = (
+        "import ctypes as C, json, sys\n"
+        f"l = C.CDLL({LIB_PATH!r})\n"
+        f"out = (C.c_double * {cap})(); order = C.c_int(0); dims = (C.c_uint64 * 16)()\n"
+        f"rc = l.ntfref_read_coo_dense({path.encode()!r}, {1 if floor is not None else 0}, "
+        f"C.c_double({float(floor or 0.0)!r}), C.c_uint64({cap}), out, C.byref(order), dims)\n"
+        "l.ntfref_last_error.restype = C.c_char_p\n"
+        "print(json.dumps([rc, l.ntfref_last_error().decode(), order.value, list(dims)[:order.value], "
+        "[float.hex(v) for v in out]]))\n")
+    rc, msg, order, shape, vals = json.loads(subprocess.run([sys.executable, "-c", code], capture_output=True,
+                                                            text=True, check=True).stdout)
+    if rc != 0:
+        raise RefError(rc, msg)
+    n = int(np.prod(shape))
+    return np.array([float.fromhex(v) for v in vals[:n]]).reshape(shape)
+
+
+def write_trace(path: str, times, losses) -> None:
+    lib().ntfref_write_trace.argtypes = [C.c_char_p, C.c_int, _P, _P]
+    t = np.ascontiguousarray(times, dtype=np.float64)
+    l = np.ascontiguousarray(losses, dtype=np.float64)
+    _check(lib().ntfref_write_trace(path.encode(), len(t), _d(t), _d(l)))

@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstring>
 #include <optional>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -455,5 +456,31 @@ SHIM int ntfref_mu_unfold_cp_sweep(int order, const std::uint64_t* dims, const d
         ntf::CpFactors f = cp_in(shape, rank, factors);
         f = ntf::mu_unfold_cp_sweep(f, tensor_in(shape, x), ntf::BetaParam(beta), eps);
         cp_out(f, factors);
+    });
+}
+
+// I/O (reference io.cpp): CTF1 write/read, COO text densify, trace CSV --
+// fixtures for the byte-exact interchange tests (tests/test_io_cpu.py).
+SHIM int ntfref_write_tensor(const char* path, int order, const std::uint64_t* dims, const double* x) {
+    return guarded([&] { ntf::write_tensor(path, tensor_in(to_shape(order, dims), x)); });
+}
+
+SHIM int ntfref_read_coo_dense(const char* path, int has_floor, double floor, std::uint64_t cap, double* out,
+                               int* order, std::uint64_t* dims) {
+    return guarded([&] {
+        const ntf::DenseTensor t =
+            ntf::read_coo(path, has_floor ? std::optional<double>(floor) : std::nullopt);
+        *order = int(t.order());
+        for (std::size_t n = 0; n < t.order(); ++n) dims[n] = t.shape()[n];
+        if (t.size() > cap) throw std::runtime_error("capacity");
+        for (std::size_t i = 0; i < t.size(); ++i) out[i] = t[i];
+    });
+}
+
+SHIM int ntfref_write_trace(const char* path, int n, const double* times, const double* losses) {
+    return guarded([&] {
+        std::vector<ntf::TraceRecord> r(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) r[std::size_t(i)] = ntf::TraceRecord{std::size_t(i), times[i], losses[i]};
+        ntf::write_trace(path, r);
     });
 }

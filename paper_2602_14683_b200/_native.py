@@ -82,6 +82,16 @@ _SIGS = {
                     C.POINTER(ShardC), _P, C.POINTER(TraceRowC), _U],
     "ntfg_cp_fit_coo": [_V, C.POINTER(FitConfigC), C.c_int32, C.c_uint32, _U, C.c_uint64, _V, _V, C.c_int32,
                         C.c_int32, _P, C.POINTER(TraceRowC), _U],
+    "ntfg_ctf1_header": [C.c_char_p, C.POINTER(C.c_uint32), _U, C.c_uint32, C.c_uint64],
+    "ntfg_ctf1_read": [_V, C.c_char_p, _V, C.c_int32, C.c_int32, C.c_uint64],
+    "ntfg_ctf1_write": [_V, C.c_char_p, C.c_uint32, _U, _V, C.c_int32, C.c_int32],
+    "ntfg_coo_text_read": [C.c_char_p, C.POINTER(C.c_uint32), _U, C.c_uint32, _U, _V, _P, C.c_uint64,
+                           C.c_uint64],
+    "ntfg_trace_write": [C.c_char_p, C.POINTER(TraceRowC), C.c_uint64],
+    "ntfg_philox_uniforms": [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _P],
+    "ntfg_cp_factors_generate": [C.c_uint32, _U, C.c_uint64, C.c_uint64, C.c_int32, C.c_double, _P],
+    "ntfg_generate_cp_gamma": [_V, C.c_uint32, _U, C.c_uint64, C.c_uint64, C.c_uint32, C.c_double, C.c_uint64,
+                               C.c_uint64, _V, C.c_int32],
     "ntfg_tucker_fit": [_V, C.POINTER(FitConfigC), C.c_int32, C.c_uint32, _U, _V, C.c_int32, C.c_int32,
                         C.POINTER(ShardC), _P, _P, C.POINTER(TraceRowC), _U],
     "ntfg_cp_reconstruct": [_V, C.c_int32, C.c_uint32, _U, C.c_uint64, _P, _P],

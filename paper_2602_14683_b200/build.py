@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xcompiler", "-fvisibility=hidden", "-I" + INCLUDE, "-I" + CSRC]
-CU_SOURCES = ["cp_api.cu", "tucker_api.cu", "capi.cu"]
+CU_SOURCES = ["cp_api.cu", "tucker_api.cu", "io_api.cu", "capi.cu"]
 CXX_API_SOURCES = ["ntf_api.cpp"]
 
 

@@ -13,6 +13,16 @@ void cp_fit(Context&, const ntfg_fit_config&, int, uint32_t, const uint64_t*, co
 void cp_fit_coo(Context&, const ntfg_fit_config&, int, uint32_t, const uint64_t*, uint64_t, const int32_t*,
                 const void*, int, int, double*, ntfg_trace_row*, uint64_t*);
 void cp_reconstruct(Context&, int, uint32_t, const uint64_t*, uint64_t, const double*, double*);
+// io_api.cu
+void ctf1_header_api(const char*, uint32_t*, uint64_t*, uint32_t, uint64_t);
+void ctf1_read(Context*, const char*, void*, int, int, uint64_t);
+void ctf1_write(Context*, const char*, uint32_t, const uint64_t*, const void*, int, int);
+void coo_text_read(const char*, uint32_t*, uint64_t*, uint32_t, uint64_t*, int32_t*, double*, uint64_t, uint64_t);
+void trace_write(const char*, const ntfg_trace_row*, uint64_t);
+void philox_uniforms(uint64_t, uint64_t, uint64_t, uint64_t, double*);
+void cp_factors_philox(uint32_t, const uint64_t*, uint64_t, uint64_t, int, double, double*);
+void generate_cp_gamma(Context&, uint32_t, const uint64_t*, uint64_t, uint64_t, uint32_t, double, uint64_t,
+                       uint64_t, void*, int);
 void cp_contract(Context&, int, uint32_t, const uint64_t*, const double*, uint64_t, const double*,
                  uint32_t, double*);
 void cp_objective(Context&, int, double, uint32_t, const uint64_t*, const double*, uint64_t,
@@ -194,6 +204,76 @@ NTFG_API ntfg_status ntfg_cp_fit_coo(ntfg_context* ctx, const ntfg_fit_config* c
     if (nnz > 0) { need(indices, "indices"); need(values, "values"); }
     ntfg::cp_fit_coo(c, *cfg, algo, order, dims, nnz, indices, values, values_dtype, location, factors, trace,
                      trace_len);
+  });
+}
+
+// ---- io / generators ----------------------------------------------------------------
+NTFG_API ntfg_status ntfg_ctf1_header(const char* path, uint32_t* order, uint64_t* dims, uint32_t cap,
+                                      uint64_t max_entries) {
+  return guard([&] {
+    need(path, "path"); need(order, "order");
+    ntfg::ctf1_header_api(path, order, dims, cap, max_entries);
+  });
+}
+
+NTFG_API ntfg_status ntfg_ctf1_read(ntfg_context* ctx, const char* path, void* dst, int32_t dtype,
+                                    int32_t location, uint64_t max_entries) {
+  return guard([&] {
+    need(path, "path"); need(dst, "dst");
+    if (ctx) ctx->activate();
+    ntfg::ctf1_read(ctx, path, dst, dtype, location, max_entries);
+  });
+}
+
+NTFG_API ntfg_status ntfg_ctf1_write(ntfg_context* ctx, const char* path, uint32_t order, const uint64_t* dims,
+                                     const void* src, int32_t dtype, int32_t location) {
+  return guard([&] {
+    need(path, "path"); need(dims, "dims"); need(src, "src");
+    if (ctx) ctx->activate();
+    ntfg::ctf1_write(ctx, path, order, dims, src, dtype, location);
+  });
+}
+
+NTFG_API ntfg_status ntfg_coo_text_read(const char* path, uint32_t* order, uint64_t* dims, uint32_t cap,
+                                        uint64_t* nnz, int32_t* indices, double* values, uint64_t capacity,
+                                        uint64_t max_entries) {
+  return guard([&] {
+    need(path, "path"); need(order, "order"); need(dims, "dims"); need(nnz, "nnz");
+    if (indices) need(values, "values");
+    ntfg::coo_text_read(path, order, dims, cap, nnz, indices, values, capacity, max_entries);
+  });
+}
+
+NTFG_API ntfg_status ntfg_trace_write(const char* path, const ntfg_trace_row* rows, uint64_t n) {
+  return guard([&] {
+    need(path, "path");
+    if (n) need(rows, "rows");
+    ntfg::trace_write(path, rows, n);
+  });
+}
+
+NTFG_API ntfg_status ntfg_philox_uniforms(uint64_t seed, uint64_t stream, uint64_t offset, uint64_t n,
+                                          double* out) {
+  return guard([&] {
+    if (n) need(out, "out");
+    ntfg::philox_uniforms(seed, stream, offset, n, out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_factors_generate(uint32_t order, const uint64_t* dims, uint64_t rank, uint64_t seed,
+                                              int32_t which, double eps, double* out) {
+  return guard([&] {
+    need(dims, "dims"); need(out, "out");
+    ntfg::cp_factors_philox(order, dims, rank, seed, which, eps, out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_generate_cp_gamma(ntfg_context* ctx, uint32_t order, const uint64_t* dims,
+                                            uint64_t rank, uint64_t seed, uint32_t gamma_k, double gamma_theta,
+                                            uint64_t row0, uint64_t row1, void* x, int32_t dtype) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(x, "x");
+    ntfg::generate_cp_gamma(c, order, dims, rank, seed, gamma_k, gamma_theta, row0, row1, x, dtype);
   });
 }
 

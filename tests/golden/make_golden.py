@@ -72,7 +72,36 @@ def main():
     out.update(cp_block("exj", x, init, "jcomm", 0.5, 25, extrapolate=True))
     out.update(cp_block("tol", x, init, "jcomm", 1.0, 500, tol=1e-6))
     save("misc.npz", **out)
+    io_fixtures()
+
+
+COO_TEXT = """
+dims: 3 4 2
+
+0 1 1 2.5
+2 3 0 1
+0 1 1 0.25
+1 0 1 4
+2 3 0 1e-3
+0 0 0 0
+"""
+
+
+def io_fixtures():
+    """CTF1 bytes, COO densify and trace CSV written by the compiled reference."""
+    x = np.array([-0.0, 5e-324, 1e308, np.pi, 1.0 / 3.0, 2.0 ** -1074, -1.5, 7.0, 0.1, 1e-300, 123456789.0,
+                  2.0 ** 52 + 1.0]).reshape(3, 2, 2)
+    R.write_tensor(os.path.join(HERE, "ref_small.ctf1"), x)
+    with open(os.path.join(HERE, "coo_small.txt"), "w") as f:
+        f.write(COO_TEXT)
+    dense = R.read_coo_dense(os.path.join(HERE, "coo_small.txt"), 64)
+    floored = R.read_coo_dense(os.path.join(HERE, "coo_small.txt"), 64, floor=0.5)
+    R.write_trace(os.path.join(HERE, "ref_trace.csv"), [0.0, 0.125, 1.0 / 3.0], [np.pi, 1e-17, 2.0 / 3.0])
+    save("io_small.npz", ctf1_values=x, coo_dense=dense, coo_dense_floor=floored)
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "io":
+        io_fixtures()
+    else:
+        main()
