@@ -144,6 +144,16 @@ ntfg_status ntfg_cp_fit_coo(ntfg_context* ctx, const ntfg_fit_config* cfg, int32
                             int32_t location, double* factors_inout, ntfg_trace_row* trace,
                             uint64_t* trace_len);
 
+/* MU-unfold baseline (reference unfold.hpp:35-37, unfold.cpp:109-135,187-197):
+ * explicit Khatri-Rao + unfolding + cuBLAS GEMMs; the comparison path for the
+ * contraction engine (acceptance criterion 2 pins sweep == bcomm_sweep). */
+ntfg_status ntfg_cp_mu_unfold_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, uint32_t order,
+                                  const uint64_t* dims, const void* x, int32_t x_dtype, int32_t x_location,
+                                  double* factors_inout, ntfg_trace_row* trace, uint64_t* trace_len);
+ntfg_status ntfg_cp_mu_unfold_sweep(ntfg_context* ctx, int32_t precision, double beta, double eps,
+                                    uint32_t order, const uint64_t* dims, const double* x, uint64_t rank,
+                                    double* factors_inout);
+
 /* ---- data ingestion and generation (reference io.hpp / io.cpp) ---------------
  * ctx may be NULL for host-only calls (location NTFG_HOST). */
 

@@ -274,3 +274,13 @@ def write_trace(path: str, times, losses) -> None:
     t = np.ascontiguousarray(times, dtype=np.float64)
     l = np.ascontiguousarray(losses, dtype=np.float64)
     _check(lib().ntfref_write_trace(path.encode(), len(t), _d(t), _d(l)))
+
+
+def mu_unfold_cp_sweep(x, factors, beta, eps=1e-12):
+    """The compiled reference's matricized sweep (unfold.cpp:109-135)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    f = _cat(factors)
+    rank = np.shape(factors[0])[1]
+    _check(lib().ntfref_mu_unfold_cp_sweep(C.c_int(x.ndim), _u64(x.shape).ctypes.data_as(_U), _d(x), C.c_int(rank),
+                                           _d(f), C.c_double(beta), C.c_double(eps)))
+    return _split(f, [np.shape(a) for a in factors])

@@ -405,6 +405,37 @@ def jcomm_fit_coo(indices, values, dims, init, cfg: FitConfig, ctx: Optional[Con
     return _cp_fit_coo(1, indices, values, dims, init, cfg, ctx)
 
 
+def mu_unfold_cp_fit(x, init, cfg: FitConfig, ctx: Optional[Context] = None) -> CpFitResult:
+    """Classical matricized MU baseline (reference unfold.cpp:187-197): explicit
+    Khatri-Rao + unfolding + cuBLAS GEMMs, for the contraction-vs-unfolding
+    comparison."""
+    ctx = ctx or default_context()
+    dims, xp, xdt, xloc, keep = _x_arg(x)
+    init = [_f64(a) for a in init]
+    cfgc, keep_r = cfg._c()
+    _check(N.load().ntfg_validate_fit_config(C.byref(cfgc)))
+    r = _check_cp_model(init, dims, "mu_unfold_cp_fit")
+    cfgc.rank = r
+    f = _cat(init)
+    rows = (N.TraceRowC * (int(cfg.max_iters) + 1))()
+    n = C.c_uint64(0)
+    _check(N.load().ntfg_cp_mu_unfold_fit(ctx.h, C.byref(cfgc), len(dims), _u64(dims).ctypes.data_as(_UP), xp, xdt,
+                                          xloc, _dp(f), rows, C.byref(n)))
+    return CpFitResult(_split(f, [a.shape for a in init]), _trace(rows, n.value))
+
+
+def mu_unfold_cp_sweep(f, x, beta: float, eps: float, precision: str = "f64", ctx=None) -> List[np.ndarray]:
+    """mu_unfold_cp_sweep (reference unfold.cpp:109-135) on the GPU."""
+    ctx = ctx or default_context()
+    x = _f64(x)
+    f = [_f64(a) for a in f]
+    r = _check_cp_model(f, list(x.shape), "mu_unfold_cp_sweep")
+    flat = _cat(f)
+    _check(N.load().ntfg_cp_mu_unfold_sweep(ctx.h, _prec(precision), float(beta), float(eps), x.ndim,
+                                            _u64(list(x.shape)).ctypes.data_as(_UP), _dp(x), r, _dp(flat)))
+    return _split(flat, [a.shape for a in f])
+
+
 # ---------------------------------------------------------------------------
 # CP step level (reference cp.hpp:30-74)
 

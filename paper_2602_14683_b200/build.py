@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xcompiler", "-fvisibility=hidden", "-I" + INCLUDE, "-I" + CSRC]
-CU_SOURCES = ["cp_api.cu", "tucker_api.cu", "io_api.cu", "capi.cu"]
+CU_SOURCES = ["cp_api.cu", "tucker_api.cu", "io_api.cu", "unfold_api.cu", "capi.cu"]
 CXX_API_SOURCES = ["ntf_api.cpp"]
 
 
@@ -69,7 +69,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 print(r.stdout + r.stderr, file=sys.stderr)
     lib = os.path.join(LIB, "libntfg.so")
     if force or jobs or _stale(lib, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcuda"])
+        _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcuda", "-lcublas"])
     # drop-in C++ API over the C ABI
     api_srcs = [os.path.join(CSRC, s) for s in CXX_API_SOURCES if os.path.exists(os.path.join(CSRC, s))]
     if api_srcs:

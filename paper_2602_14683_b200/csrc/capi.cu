@@ -13,6 +13,10 @@ void cp_fit(Context&, const ntfg_fit_config&, int, uint32_t, const uint64_t*, co
 void cp_fit_coo(Context&, const ntfg_fit_config&, int, uint32_t, const uint64_t*, uint64_t, const int32_t*,
                 const void*, int, int, double*, ntfg_trace_row*, uint64_t*);
 void cp_reconstruct(Context&, int, uint32_t, const uint64_t*, uint64_t, const double*, double*);
+// unfold_api.cu
+void cp_mu_unfold_fit(Context&, const ntfg_fit_config&, uint32_t, const uint64_t*, const void*, int, int, double*,
+                      ntfg_trace_row*, uint64_t*);
+void cp_mu_unfold_sweep(Context&, int, double, double, uint32_t, const uint64_t*, const double*, uint64_t, double*);
 // io_api.cu
 void ctf1_header_api(const char*, uint32_t*, uint64_t*, uint32_t, uint64_t);
 void ctf1_read(Context*, const char*, void*, int, int, uint64_t);
@@ -204,6 +208,25 @@ NTFG_API ntfg_status ntfg_cp_fit_coo(ntfg_context* ctx, const ntfg_fit_config* c
     if (nnz > 0) { need(indices, "indices"); need(values, "values"); }
     ntfg::cp_fit_coo(c, *cfg, algo, order, dims, nnz, indices, values, values_dtype, location, factors, trace,
                      trace_len);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_mu_unfold_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, uint32_t order,
+                                           const uint64_t* dims, const void* x, int32_t x_dtype, int32_t x_location,
+                                           double* factors, ntfg_trace_row* trace, uint64_t* trace_len) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(cfg, "cfg"); need(dims, "dims"); need(x, "x"); need(factors, "factors");
+    need(trace, "trace"); need(trace_len, "trace_len");
+    ntfg::cp_mu_unfold_fit(c, *cfg, order, dims, x, x_dtype, x_location, factors, trace, trace_len);
+  });
+}
+
+NTFG_API ntfg_status ntfg_cp_mu_unfold_sweep(ntfg_context* ctx, int32_t precision, double beta, double eps,
+                                             uint32_t order, const uint64_t* dims, const double* x, uint64_t rank,
+                                             double* factors) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(x, "x"); need(factors, "factors");
+    ntfg::cp_mu_unfold_sweep(c, precision, beta, eps, order, dims, x, rank, factors);
   });
 }
 
