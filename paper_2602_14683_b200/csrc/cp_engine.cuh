@@ -19,6 +19,7 @@
 #include "cp_kernels.cuh"
 #include "engine.cuh"
 #include "stream3_kernels.cuh"
+#include "recon_tile.cuh"
 #include "tc_contract.cuh"
 
 namespace ntfg {
@@ -76,7 +77,7 @@ class CpEngine {
     raw_ = c_.buf<double>("cp.raw", 1);
     numden_ = c_.buf<double>("cp.numden", size_t(2) * max_dim() * R_);
     // objective partials: one per recon CTA (grid depends on the kernel variant)
-    objpart_ = c_.buf<double>("cp.objpart", size_t(std::max(recon_grid(false), recon_grid(true))));
+    objpart_ = c_.buf<double>("cp.objpart", size_t(std::max({recon_grid(false), recon_grid(true), c_.sm_count * 8})));
     tc_ = decide_tc();
   }
 
@@ -240,7 +241,26 @@ class CpEngine {
     p.beta = beta_;
     p.eps = eps_;
     p.bk = bk_;
-    obj_split_ = planes_out_ && split_objective();
+    // tensor-core path (fp32, K % 128 == 0): the register-tiled kernel for the
+    // planes pass and for objective-only passes
+    const bool tile = tc_ && sizeof(T) == 4 && !htab && !xhout && !pout && !qout && rows_tma_ok(x_) &&
+                      g_.K % kRtCols == 0 && RP_ <= 64 && !tile_disabled();
+    obj_split_ = tile ? split_objective() : (planes_out_ && split_objective());
+    if (tile) {
+      p.ktiles = int(g_.K / kRtCols);
+      const int ph = c_.prof_begin(0);
+      if constexpr (sizeof(T) == 4) {
+        switch (RP_) {
+          case 8: launch_tile<8>(p); break;
+          case 16: launch_tile<16>(p); break;
+          case 32: launch_tile<32>(p); break;
+          default: launch_tile<64>(p); break;
+        }
+      }
+      c_.prof_end(ph);
+      if (objective) finish_objective();
+      return;
+    }
     const bool v3 = (rows_tma_ok(x_) && (!pout || rows_tma_ok(pout)) && (!qout || rows_tma_ok(qout))) || planes_out_;
     recon_grid_ = recon_grid(v3);
     recon_v3_ = v3;
@@ -300,6 +320,45 @@ class CpEngine {
     return true;
   }
   int tc_n() const { return R_ <= 16 ? 16 : R_ <= 32 ? 32 : 64; }
+  // shared-memory plan of one contraction launch: A stages (1024-aligned),
+  // B tiles, then the B producers' cp.async gather ring.  Deeper gathers first
+  // (they hide the L2 latency of the factor rows), then more stages.
+  TcLayout tc_layout(int ns, int N, int nmm) const {
+    TcLayout L{};
+    L.a_stream = uint32_t(2 * (g_.K / 64) * 2048);
+    L.a_stage = uint32_t(ns) * L.a_stream;
+    L.b_tile = uint32_t(N / 8 * kTcBSbo);
+    L.gmodes = std::max(1, std::min(nmm, kTcGModes));
+    const size_t ring_per = size_t(ns) * L.gmodes * 16 * N * 4;  // [slot][ns][gmodes][16 rows][N]
+    auto total = [&](int nst, int gd) {
+      return size_t(nst) * L.a_stage + size_t(nst) * 4 * L.b_tile + size_t(gd) * ring_per + 1024;
+    };
+    int nst = 3, gd = 2;
+    if (total(nst, gd) > kTcSmemMax) nst = 2;
+    while (gd < 4 && total(nst, gd + 1) <= kTcSmemMax) ++gd;
+    static_assert(kTcMaxGather >= 4, "gather ring depth");
+    while (nst < kTcMaxStages && total(nst + 1, gd) <= kTcSmemMax) ++nst;
+    if (total(nst, gd) > kTcSmemMax) throw Error(NTFG_ERR_SHAPE, "tensor-core contraction: shared memory plan");
+    L.nst = nst;
+    L.gdepth = gd;
+    L.b_off = uint32_t(nst) * L.a_stage;
+    L.ring_off = L.b_off + uint32_t(nst) * 4 * L.b_tile;
+    L.total = uint32_t(total(nst, gd));
+    return L;
+  }
+  template <typename KF>
+  void launch_tc(KF kern, int grid, const TcMaps& maps, const TcParams& p) {
+    static std::mutex mu;
+    static std::set<const void*> done;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (done.insert(reinterpret_cast<const void*>(kern)).second)
+        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemMax)),
+                   "cudaFuncSetAttribute");
+    }
+    kern<<<grid, 352, p.lay.total, c_.stream>>>(maps, p);
+    NTFG_LAUNCHED(c_);
+  }
   bool tc() const { return tc_; }
   void disable_tc() { tc_allowed_ = false; tc_ = false; }
   void* plane(int i) { ensure_pq(); return planes_[i]; }
@@ -347,20 +406,39 @@ class CpEngine {
       mapA = An;
     }
     p.fB.init(p.Bn);
+    // fp32 zero-padded copies of every factor of every stream (B gathers, case-B epilogue)
+    F32Stage fs{};
+    fs.order = N_;
+    fs.ns = ns;
+    fs.R = int(R_);
+    fs.N = p.N;
+    for (int m = 0; m < N_; ++m) fs.off[m + 1] = fs.off[m] + g_.dims[m] * p.N;
+    if (!lastT_) lastT_ = c_.buf<float>("cp.lastT", size_t(2) * fs.off[N_]);
     for (int s = 0; s < ns; ++s) {
-      for (int m = 0; m < N_; ++m) p.mfac[s][m] = st[s].fac[m];
-      if (!caseA) {
-        if (!lastT_) lastT_ = c_.buf<float>("cp.lastT", size_t(2) * g_.K * 64);
-        float* lt = lastT_ + size_t(s) * g_.K * p.N;
-        pad_last_kernel<<<int(ceil_div(g_.K * p.N, 256)), 256, 0, c_.stream>>>(st[s].fac[N_ - 1], g_.K, int(R_),
-                                                                               p.N, lt);
-        NTFG_LAUNCHED(c_);
-        p.lastfac[s] = lt;
+      for (int m = 0; m < N_; ++m) {
+        p.mfac[s][m] = st[s].fac[m];
+        fs.src[s][m] = st[s].fac[m];
+        fs.dst[s][m] = lastT_ + size_t(s) * fs.off[N_] + fs.off[m];
+        p.fac32[s][m] = fs.dst[s][m];
       }
+      p.lastfac[s] = p.fac32[s][N_ - 1];
       for (int h = 0; h < 2; ++h)
         if (!tc::make_plane_map(&maps.m[s][h], planes_[2 * st[s].plane + h], g_.K, mapB, mapI, mapA, p.boxB,
                                 p.boxA))
           throw Error(NTFG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    }
+    stage_f32_kernel<<<int(std::min<int64_t>(ceil_div(fs.off[N_] * ns, 256), 1024)), 256, 0, c_.stream>>>(fs);
+    NTFG_LAUNCHED(c_);
+    int nmm = 0;
+    for (int m = 0; m < N_ - 1; ++m) nmm += (m != n);
+    p.lay = tc_layout(ns, p.N, nmm);
+    {  // fast gathers: the fastest off-mode f (highest index != n among the row modes) has 16 | I_f
+      int f = -1;
+      for (int m = 0; m < N_ - 1; ++m)
+        if (m != n) f = m;
+      p.gfast = (f >= 0 && g_.dims[f] % kTcRows == 0) ? 1 : 0;
+      static const bool slow = [] { const char* e = std::getenv("NTFG_TC_SLOW_GATHER"); return e && e[0] == '1'; }();
+      if (slow) p.gfast = 0;
     }
     p.partA = reinterpret_cast<float*>(partA_);
     p.partB = partB_;
@@ -376,21 +454,24 @@ class CpEngine {
     const int grid = int(std::min<int64_t>(p.units, int64_t(c_.sm_count)));
     static const char* trace_path = std::getenv("NTFG_TC_TRACE");  // perf experiments (eager fits only)
     if (trace_path) {
-      p.trace = reinterpret_cast<unsigned long long*>(c_.bufs.get("cp.tctrace", size_t(grid) * 16 * 8 * 8));
-      NTFG_CUDA(cudaMemsetAsync(p.trace, 0, size_t(grid) * 16 * 8 * 8, c_.stream));
+      p.trace = reinterpret_cast<unsigned long long*>(c_.bufs.get("cp.tctrace", size_t(grid) * 17 * 8 * 8));
+      NTFG_CUDA(cudaMemsetAsync(p.trace, 0, size_t(grid) * 17 * 8 * 8, c_.stream));
     }
-    if (p.N == 16) launch_dyn(tc_contract_kernel<16>, dim3(grid), dim3(320), TcSmem<16>::total, maps, p);
-    else if (p.N == 32) launch_dyn(tc_contract_kernel<32>, dim3(grid), dim3(320), TcSmem<32>::total, maps, p);
-    else launch_dyn(tc_contract_kernel<64>, dim3(grid), dim3(320), TcSmem<64>::total, maps, p);
+    if (p.N == 16) launch_tc(tc_contract_kernel<16>, grid, maps, p);
+    else if (p.N == 32) launch_tc(tc_contract_kernel<32>, grid, maps, p);
+    else launch_tc(tc_contract_kernel<64>, grid, maps, p);
     if (trace_path) {
-      std::vector<unsigned long long> h(size_t(grid) * 16 * 8);
+      std::vector<unsigned long long> h(size_t(grid) * 17 * 8);
       NTFG_CUDA(cudaMemcpyAsync(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost, c_.stream));
       NTFG_CUDA(cudaStreamSynchronize(c_.stream));
       if (FILE* f = std::fopen(trace_path, "a")) {
         std::fprintf(f, "launch n=%d units=%lld S=%lld grid=%d\n", n, (long long)p.units, (long long)p.S, grid);
-        for (size_t i = 0; i < h.size(); i += 8)
+        for (size_t i = 0; i < size_t(grid) * 128; i += 8)
           std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 128, (i / 8) % 16, h[i], h[i + 1],
                        h[i + 2], h[i + 3], h[i + 4], h[i + 5], h[i + 6], h[i + 7]);
+        for (size_t i = size_t(grid) * 128; i < h.size(); i += 8)  // per-CTA role wait totals
+          std::fprintf(f, "wstats %llu %llu %llu %llu %llu %llu %llu\n", h[i], h[i + 1], h[i + 2], h[i + 3],
+                       h[i + 4], h[i + 5], h[i + 6]);
         std::fclose(f);
       }
     }
@@ -456,7 +537,11 @@ class CpEngine {
     partB_ = c_.buf<double>("cp.partB", std::max<size_t>(b, 1));
     partAd_ = c_.buf<double>("cp.partAd", std::max<size_t>(a / 8 + size_t(ns) * g_.K * RP_, 1));
     if (beta_ == 1.0) n1num_ = c_.buf<double>("cp.n1num", factor_doubles() + size_t(max_dim()) * R_);
-    if (tc_) lastT_ = c_.buf<float>("cp.lastT", size_t(2) * g_.K * 64);
+    if (tc_) {
+      size_t fl = 0;
+      for (int m = 0; m < N_; ++m) fl += size_t(g_.dims[m]) * 64;
+      lastT_ = c_.buf<float>("cp.lastT", 2 * fl);
+    }
     ensure_pq();
   }
 
@@ -963,6 +1048,55 @@ class CpEngine {
     NTFG_LAUNCHED(c_);
   }
 
+  static bool tile_disabled() {  // perf experiments: NTFG_DISABLE_RTILE=1 keeps recon3
+    static const bool v = [] { const char* e = std::getenv("NTFG_DISABLE_RTILE"); return e && e[0] == '1'; }();
+    return v;
+  }
+  template <int RP, int BK, int NPRE>
+  void launch_tile_np(const ReconParams<float>& p) {
+    constexpr size_t sm = RtSmem<RP>::total;
+    static int per_sm = 0;
+    static std::mutex mu;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (!per_sm) {
+        cuda_check(cudaFuncSetAttribute(recon_tile_kernel<RP, BK, NPRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(sm)), "cudaFuncSetAttribute");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, recon_tile_kernel<RP, BK, NPRE>, kRtThreads,
+                                                                 sm),
+                   "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+        per_sm = std::max(1, std::min(per_sm, 4));
+      }
+    }
+    const int64_t ntiles = ceil_div(g_.rows, int64_t(kRtRows));
+    const int64_t per = std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(c_.sm_count) * per_sm / p.ktiles));
+    recon_grid_ = int(per * p.ktiles);
+    recon_tile_kernel<RP, BK, NPRE><<<recon_grid_, kRtThreads, sm, c_.stream>>>(p);
+    NTFG_LAUNCHED(c_);
+  }
+  template <int RP, int BK>
+  void launch_tile_bk(const ReconParams<float>& p) {
+    // fast H: 1..3 row modes, the fastest with 32 | I (tiles never straddle its blocks)
+    const int npre = N_ - 1;
+    const bool fast = npre >= 1 && npre <= 3 && g_.dims[npre - 1] % kRtRows == 0;
+    if (!fast) launch_tile_np<RP, BK, 0>(p);
+    else if (npre == 1) launch_tile_np<RP, BK, 1>(p);
+    else if (npre == 2) launch_tile_np<RP, BK, 2>(p);
+    else launch_tile_np<RP, BK, 3>(p);
+  }
+  template <int RP>
+  void launch_tile(const ReconParams<T>& pp) {
+    if constexpr (sizeof(T) == 4) {
+      const ReconParams<float>& p = pp;
+      switch (bk_) {
+        case kBeta1: launch_tile_bk<RP, kBeta1>(p); break;
+        case kBetaHalf: launch_tile_bk<RP, kBetaHalf>(p); break;
+        case kBeta3Half: launch_tile_bk<RP, kBeta3Half>(p); break;
+        case kBeta0: launch_tile_bk<RP, kBeta0>(p); break;
+        default: launch_tile_bk<RP, kBetaGeneric>(p); break;
+      }
+    }
+  }
   template <int RP>
   void launch_recon(const ReconParams<T>& p) {
     constexpr int KT2 = (sizeof(T) == 4 && RP <= 32) ? 2 : 1;

@@ -44,6 +44,17 @@ __device__ __forceinline__ void wait(uint64_t* bar, unsigned phase) {
       : "memory");
 }
 
+// ---- shared-space loads/stores (32-bit shared addresses) -----------------------
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_v4(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
 // ---- TMA --------------------------------------------------------------------------
 __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
                                             int c4, uint64_t* bar) {

@@ -12,12 +12,24 @@
 // cross-unit reductions stay fp64 (hard part 2).  Same 8 bytes
 // per entry per pass as fp32 P~/Q~.
 //
-// Warp roles (320 threads): 0-3 build the B tiles (M rows, fp64 factor
-// gathers one stage ahead), 4-7 epilogue (tcgen05.ld -> partials), 8 TMA
-// producer, 9 TMEM allocator + single-thread MMA issuer.  Stages of 16 rows
-// cycle through a 3-deep smem ring guarded by mbarriers (TMA tx, B-tile
-// arrivals, tcgen05.commit); the TMEM accumulator is double-buffered across
-// units when it fits so the epilogue of one unit overlaps the next.
+// Warp roles (352 threads): 0-3 build the B tiles (M rows), 4-7 epilogue
+// (tcgen05.ld -> partials), 8 TMA producer, 9 TMEM allocator + single-thread
+// MMA issuer, 10 factor-row gathers.  Stages of 16 rows cycle through a smem ring (2-6 deep, sized
+// from K at launch) guarded by mbarriers (TMA tx, B-tile arrivals,
+// tcgen05.commit); the TMEM accumulator is double-buffered across units when
+// it fits so the epilogue of one unit overlaps the next.
+//
+// B producers: each thread owns one stage row and W = N/8 rank columns.  The
+// factor rows it multiplies come from fp32 zero-padded copies of the factors
+// (stage_f32_kernel, one launch per contraction), gathered by warp 10 with
+// bulk async copies (async proxy, mbarrier completion) into a smem ring
+// `gdepth` stages ahead of the MMA.  Keeping the gathers out of the B threads
+// matters twice: their L2 latency leaves the stage cadence, and the B
+// threads' per-stage fence.proxy.async no longer waits for in-flight loads
+// (register or cp.async gathers in the B threads made a K = 256 / R = 64
+// stage take ~3 us -- 23% of HBM -- on C5).  B tiles use a 272-byte stride between
+// 8-column core-matrix groups (SBO) so the 2-byte stores of one warp hit 16
+// distinct banks instead of 2.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -27,8 +39,22 @@
 
 namespace ntfg {
 
-constexpr int kTcRows = 16;   // UMMA K for 16-bit inputs
-constexpr int kTcStages = 3;
+constexpr int kTcRows = 16;     // UMMA K for 16-bit inputs
+constexpr int kTcMaxStages = 6;
+constexpr int kTcMaxGather = 6;
+constexpr int kTcBSbo = 272;    // bytes between 8-column groups of a B tile (256 + 16: bank spread)
+constexpr int kTcGModes = 3;    // factor modes gathered through the cp.async ring (more: direct fp64)
+constexpr size_t kTcSmemMax = 227 * 1024 - 2560;  // dynamic budget (static smem 2.3 KB)
+
+// runtime shared-memory layout (host-computed, tc_layout)
+struct TcLayout {
+  uint32_t a_stream, a_stage;  // bytes of one stream's A planes / all streams (multiple of 1024)
+  uint32_t b_tile;             // bytes of one bf16 B tile
+  uint32_t b_off, ring_off;    // region offsets
+  int nst, gdepth, gmodes;     // stages, gather ring depth, gathered modes
+
+  uint32_t total;
+};
 
 struct TcParams {
   Geom g;
@@ -42,6 +68,9 @@ struct TcParams {
   const double* mfac[2][kMaxOrder];
   const float* lastfac[2];   // case B: last-mode factor as [K][N] fp32, zero padded past R (G itself
                              // is an fp32 MMA result, so fp32 F adds ~6e-8 per term)
+  const float* fac32[2][kMaxOrder];  // every factor as [I_m][N] fp32, zero padded (B operand gathers)
+  int gfast;                          // stage rows = 16 consecutive rows of the fastest off-mode
+  TcLayout lay;
   float* partA;          // [ns][units][K][RP]
   double* partB;         // [ns][In][S][RP]
   int tmem_cols, dbuf;   // allocation, double-buffered accumulator?
@@ -53,15 +82,11 @@ struct TcMaps {
   CUtensorMap m[2][2];  // [stream][hi, lo]
 };
 
-template <int NMAX>
-struct TcSmem {
-  static constexpr size_t a_stream = size_t(2) * 4 * 2 * 2048;  // hi/lo x 4 m-tiles x 2 ko blocks (max)
-  static constexpr size_t a_stage = 2 * a_stream;                // two streams
-  static constexpr size_t b_tile = size_t(NMAX) * kTcRows * 2;   // one bf16 B tile
-  static constexpr size_t b_stage = 2 * 2 * b_tile;               // [stream][hi, lo]
-  static constexpr size_t stage = a_stage + b_stage;
-  static constexpr size_t total = kTcStages * stage + 1024;       // + alignment slack
-};
+// two values -> packed bf16 hi and lo (element a in the low half)
+__device__ __forceinline__ void bf16_split_pair_fast(float a, float b, uint32_t& hi, uint32_t& lo) {
+  hi = bf16x2_bits(__floats2bfloat162_rn(a, b));
+  lo = bf16x2_bits(__floats2bfloat162_rn(a - bf16_lo_f(hi), b - bf16_hi_f(hi)));
+}
 
 __device__ __forceinline__ void bf16_split(double v, __nv_bfloat16& hi, __nv_bfloat16& lo) {
   const float f = float(v);
@@ -70,12 +95,13 @@ __device__ __forceinline__ void bf16_split(double v, __nv_bfloat16& hi, __nv_bfl
 }
 
 template <int NMAX>
-static __global__ void __launch_bounds__(320, 1)
+static __global__ void __launch_bounds__(352, 1)
     tc_contract_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
-  using L = TcSmem<NMAX>;
+  const TcLayout& L = p.lay;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t a_full[kTcStages], b_full[kTcStages], empty[kTcStages], acc_full[2], acc_empty[2];
+  __shared__ uint64_t a_full[kTcMaxStages], b_full[kTcMaxStages], empty[kTcMaxStages], acc_full[2], acc_empty[2];
+  __shared__ uint64_t g_full[kTcMaxGather], g_empty[kTcMaxGather];
   __shared__ uint32_t tmem_base;
   __shared__ double red[4][64];
 
@@ -85,10 +111,14 @@ static __global__ void __launch_bounds__(320, 1)
   constexpr int N = NMAX;  // UMMA N (host launches the instance matching the rank)
 
   if (tid == 0) {
-    for (int s = 0; s < kTcStages; ++s) {
+    for (int s = 0; s < L.nst; ++s) {
       tc::mbar_init(&a_full[s], 1);
       tc::mbar_init(&b_full[s], 128);
       tc::mbar_init(&empty[s], 1);
+    }
+    for (int g = 0; g < L.gdepth; ++g) {
+      tc::mbar_init(&g_full[g], 1);
+      tc::mbar_init(&g_empty[g], 128);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&acc_full[b], 1);
@@ -128,10 +158,10 @@ static __global__ void __launch_bounds__(320, 1)
     return aa * (In * p.Bn) + itgt * p.Bn + (j - aa * p.Bn);
   };
   auto stage_a = [&](int slot, int s, int plane) -> unsigned char* {
-    return smem + size_t(slot) * L::stage + size_t(s) * L::a_stream + size_t(plane) * (L::a_stream / 2);
+    return smem + size_t(slot) * L.a_stage + size_t(s) * L.a_stream + size_t(plane) * (L.a_stream / 2);
   };
   auto stage_b = [&](int slot, int s, int plane) -> unsigned char* {
-    return smem + size_t(slot) * L::stage + L::a_stage + (size_t(s) * 2 + plane) * L::b_tile;
+    return smem + L.b_off + ((size_t(slot) * 2 + s) * 2 + plane) * L.b_tile;
   };
 
   if (warp == 8) {
@@ -139,12 +169,15 @@ static __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       uint32_t q = 0;
       const unsigned bytes = unsigned(p.ns) * 2u * unsigned(K / 64) * 2048u;
+      unsigned long long tw = 0, t00 = p.trace ? clock64() : 0;
       for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
         int64_t j0, j1, itgt, split;
         unit_range(u, j0, j1, itgt, split);
         for (int64_t j = j0; j < j1; j += kTcRows, ++q) {
-          const int slot = int(q % kTcStages);
-          tc::wait(&empty[slot], ((q / kTcStages) & 1u) ^ 1u);
+          const int slot = int(q % unsigned(L.nst));
+          const unsigned long long tq = p.trace ? clock64() : 0;
+          tc::wait(&empty[slot], ((q / unsigned(L.nst)) & 1u) ^ 1u);
+          if (p.trace) tw += clock64() - tq;
           tc::expect_tx(&a_full[slot], bytes);
           int c2, c3, c4;
           if (p.caseA) {
@@ -157,6 +190,10 @@ static __global__ void __launch_bounds__(320, 1)
             for (int plane = 0; plane < 2; ++plane)
               tc::tma_load_5d(stage_a(slot, s, plane), &maps.m[s][plane], 0, c2, c3, c4, 0, &a_full[slot]);
         }
+      }
+      if (p.trace) {
+        p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 5] = tw;
+        p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 6] = clock64() - t00;
       }
     }
   } else if (warp == 9) {
@@ -177,8 +214,8 @@ static __global__ void __launch_bounds__(320, 1)
         unsigned long long wa = 0, wb = 0;
         bool first = true;
         for (int64_t j = j0; j < j1; j += kTcRows, ++q) {
-          const int slot = int(q % kTcStages);
-          const uint32_t ph = (q / kTcStages) & 1u;
+          const int slot = int(q % unsigned(L.nst));
+          const uint32_t ph = (q / unsigned(L.nst)) & 1u;
           unsigned long long t0 = tr ? clock64() : 0;
           tc::wait(&a_full[slot], ph);
           unsigned long long t1 = tr ? clock64() : 0;
@@ -189,8 +226,8 @@ static __global__ void __launch_bounds__(320, 1)
           }
           tc::fence_after_sync();
           for (int s = 0; s < p.ns && !(p.ablate & 2); ++s) {
-            const uint64_t bh = tc::desc_k_interleave(stage_b(slot, s, 0), 128, 256);
-            const uint64_t bl = tc::desc_k_interleave(stage_b(slot, s, 1), 128, 256);
+            const uint64_t bh = tc::desc_k_interleave(stage_b(slot, s, 0), 128, kTcBSbo);
+            const uint64_t bl = tc::desc_k_interleave(stage_b(slot, s, 1), 128, kTcBSbo);
             for (int m = 0; m < p.mt; ++m) {
               const uint32_t d = tmem + tb * uint32_t(cols_per_buf) + uint32_t((s * p.mt + m) * N);
               const uint64_t ah = tc::desc_mn_sw128(stage_a(slot, s, 0) + size_t(m) * 4096, 2048, 1024);
@@ -211,76 +248,166 @@ static __global__ void __launch_bounds__(320, 1)
         }
       }
     }
-  } else if (warp < 4) {
-    // ================= B-tile (M rows) producers =================
-    // thread t owns stage row k = t / 8 and rank columns [c*W, c*W + W),
-    // c = t % 8: the row's coordinates are decoded once and each factor row
-    // segment is a contiguous fp64 load; the gathers for the next stage are
-    // issued before this stage's MMAs wait on them (one stage of slack).
-    constexpr int W = N / 8;
-    const int k = tid >> 3, r0 = (tid & 7) * W;
+  } else if (warp == 10) {
+    // ================= factor-row gathers (bulk async copies) =================
+    // gather slot q % gdepth holds, per stream, gm regions of [16][N] floats.
+    // Fast path (p.gfast: the fastest off-mode f has 16 | I_f, so a stage's 16
+    // rows share every other coordinate and run over 16 consecutive rows of
+    // A_f): region 0 = those 16 rows (one contiguous copy), region mi > 0 =
+    // the single row of the mi-th other mode.  Otherwise one copy per
+    // (row, mode); rows past the unit end copy the unit's last row (the B
+    // threads zero them).
     const int nrm = p.g.order - 1;
     int mm[kMaxOrder];
     int nmm = 0;
     for (int m = 0; m < nrm; ++m)
       if (m != p.n) mm[nmm++] = m;
-    double pv[2][3][W];
-    auto gather = [&](int64_t j, int64_t j1, int64_t itgt) {
-#pragma unroll
-      for (int s = 0; s < 2; ++s)
-#pragma unroll
-        for (int c2 = 0; c2 < 3; ++c2)
-#pragma unroll
-          for (int w = 0; w < W; ++w) pv[s][c2][w] = (c2 == 0 && j >= j1) ? 0.0 : 1.0;
-      if (j >= j1) return;
-      const int64_t row = row_of(j, itgt);
-#pragma unroll
-      for (int c2 = 0; c2 < 3; ++c2) {
-        if (c2 >= nmm) break;
-        const int64_t crd = p.g.coord(row, mm[c2]);
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          if (s >= p.ns) break;
-          const double* f = p.mfac[s][mm[c2]] + crd * p.R + r0;
-#pragma unroll
-          for (int w = 0; w < W; ++w) pv[s][c2][w] = (r0 + w < p.R) ? __ldg(f + w) : 0.0;
+    const int gm = nmm < kTcGModes ? nmm : kTcGModes;
+    const int fm = nmm > 0 ? mm[nmm - 1] : 0;  // fastest off-mode (highest index)
+    const unsigned rowb = unsigned(N * 4);
+    const unsigned regb = 16u * rowb;
+    const unsigned bytes = p.gfast ? unsigned(p.ns) * (regb + unsigned(gm - 1) * rowb)
+                                   : unsigned(16 * gm * p.ns) * rowb;
+    unsigned char* ring = smem + L.ring_off;
+    uint32_t q = 0;
+    unsigned long long gw = 0, g00 = p.trace ? clock64() : 0;
+    if (gm > 0 && !(p.ablate & 1)) {
+      for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+        int64_t j0, j1, itgt, split;
+        unit_range(u, j0, j1, itgt, split);
+        for (int64_t jb = j0; jb < j1; jb += kTcRows, ++q) {
+          const int gs = int(q % unsigned(L.gdepth));
+          const unsigned long long tq = p.trace ? clock64() : 0;
+          tc::wait(&g_empty[gs], ((q / unsigned(L.gdepth)) & 1u) ^ 1u);
+          if (p.trace) gw += clock64() - tq;
+          if (lane == 0) tc::expect_tx(&g_full[gs], bytes);
+          __syncwarp();
+          if (p.gfast) {
+            if (lane < gm * p.ns) {
+              const int mi = lane % gm, st = lane / gm;
+              const int64_t row = row_of(jb, itgt);
+              unsigned char* dst = ring + (size_t(gs * p.ns + st) * gm + mi) * regb;
+              if (mi == 0)
+                tma::bulk_g2s(dst, p.fac32[st][fm] + p.g.coord(row, fm) * N, regb, &g_full[gs]);
+              else
+                tma::bulk_g2s(dst, p.fac32[st][mm[mi - 1]] + p.g.coord(row, mm[mi - 1]) * N, rowb, &g_full[gs]);
+            }
+          } else {
+            for (int c = lane; c < 16 * gm * p.ns; c += 32) {
+              const int kk = c & 15, mi = (c >> 4) % gm, st = (c >> 4) / gm;
+              const int64_t j = jb + kk < j1 ? jb + kk : j1 - 1;
+              const int64_t crd = p.g.coord(row_of(j, itgt), mm[mi]);
+              unsigned char* dst = ring + ((size_t(gs * p.ns + st) * gm + mi) * 16 + kk) * rowb;
+              tma::bulk_g2s(dst, p.fac32[st][mm[mi]] + crd * N, rowb, &g_full[gs]);
+            }
+          }
         }
       }
-    };
+    }
+    if (p.trace && lane == 0) {
+      p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 3] = gw;
+      p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 4] = clock64() - g00;
+    }
+  } else if (warp < 4) {
+    // ================= B-tile (M rows) producers =================
+    // work item = (stream s, k group kg of 8 stage rows, rank column r): the
+    // 8 products M(8kg..8kg+7, r) are one 16-byte core-matrix row of the
+    // K-major B tile, written as one st.shared.v4 per plane.  A warp covers
+    // 32 consecutive r: ring reads and tile stores are conflict-free.  The
+    // factor rows come from the gather ring (warp 10).
+    const int nrm = p.g.order - 1;
+    int mm[kMaxOrder];
+    int nmm = 0;
+    for (int m = 0; m < nrm; ++m)
+      if (m != p.n) mm[nmm++] = m;
+    const int gm = nmm < kTcGModes ? nmm : kTcGModes;
+    const uint32_t ring = tc::saddr(smem + L.ring_off);
+    const uint32_t btiles = tc::saddr(smem + L.b_off);
+    const int nitems = p.ns * 2 * N;
+    constexpr int kMaxItems = 2;  // ns * 2 * N <= 256
     uint32_t q = 0;
+    unsigned long long bw0 = 0, bw1 = 0, b00 = p.trace ? clock64() : 0;
     for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
       int64_t j0, j1, itgt, split;
       unit_range(u, j0, j1, itgt, split);
-      if (!(p.ablate & 1)) gather(j0 + k, j1, itgt);
       for (int64_t jb = j0; jb < j1; jb += kTcRows, ++q) {
-        const int slot = int(q % kTcStages);
-        tc::wait(&empty[slot], ((q / kTcStages) & 1u) ^ 1u);
+        const int slot = int(q % unsigned(L.nst));
         if (p.ablate & 1) {
+          tc::wait(&empty[slot], ((q / unsigned(L.nst)) & 1u) ^ 1u);
           tc::arrive(&b_full[slot]);
           continue;
         }
+        const int gs = int(q % unsigned(L.gdepth));
+        const int nvalid = int(j1 - jb < kTcRows ? j1 - jb : kTcRows);
+        unsigned long long tq = p.trace ? clock64() : 0;
+        if (gm > 0) tc::wait(&g_full[gs], (q / unsigned(L.gdepth)) & 1u);
+        if (p.trace) { bw0 += clock64() - tq; }
+        uint4 hv[kMaxItems], lv[kMaxItems];
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          if (s >= p.ns) break;
+        for (int it = 0; it < kMaxItems; ++it) {
+          const int i = tid + it * 128;
+          if (i >= nitems) break;
+          const int r = i % N, kg = (i / N) & 1, st = i / (2 * N);
+          float v[8];
 #pragma unroll
-          for (int w = 0; w < W; ++w) {
-            double v = pv[s][0][w] * pv[s][1][w] * pv[s][2][w];
-            if (nmm > 3 && jb + k < j1 && r0 + w < p.R) {  // order > 5: remaining modes here
-              const int64_t row = row_of(jb + k, itgt);
-              for (int c2 = 3; c2 < nmm; ++c2) v *= p.mfac[s][mm[c2]][p.g.coord(row, mm[c2]) * p.R + r0 + w];
+          for (int kk = 0; kk < 8; ++kk) v[kk] = kg * 8 + kk < nvalid ? 1.f : 0.f;
+          const uint32_t reg0 = ring + uint32_t((gs * p.ns + st) * gm) * 16u * uint32_t(N * 4) + uint32_t(r) * 4;
+          if (p.gfast && gm > 0) {  // v = (prod of the other modes' rows, ascending) * A_f rows
+            float g = 1.f;
+            for (int mi = 1; mi < gm; ++mi) {
+              const float f = tc::lds_f32(reg0 + uint32_t(mi) * 16u * uint32_t(N * 4));
+              g = mi == 1 ? f : g * f;
             }
-            __nv_bfloat16 hi, lo;
-            bf16_split(v, hi, lo);
-            const int r = r0 + w;
-            const size_t off = size_t(r / 8) * 256 + size_t(k / 8) * 128 + size_t(r % 8) * 16 + size_t(k % 8) * 2;
-            *reinterpret_cast<__nv_bfloat16*>(stage_b(slot, s, 0) + off) = hi;
-            *reinterpret_cast<__nv_bfloat16*>(stage_b(slot, s, 1) + off) = lo;
+            const uint32_t base = reg0 + uint32_t(kg * 8) * uint32_t(N * 4);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const float f = tc::lds_f32(base + uint32_t(kk) * uint32_t(N * 4));
+              v[kk] *= gm > 1 ? g * f : f;
+            }
+          } else {
+            for (int mi = 0; mi < gm; ++mi) {
+              const uint32_t base = reg0 + uint32_t(mi * 16 + kg * 8) * uint32_t(N * 4);
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) v[kk] *= tc::lds_f32(base + uint32_t(kk) * uint32_t(N * 4));
+            }
           }
+          if (nmm > kTcGModes) {  // order > 5: remaining modes straight from the fp64 factors
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              if (kg * 8 + kk >= nvalid) continue;
+              const int64_t row = row_of(jb + kg * 8 + kk, itgt);
+              for (int c2 = kTcGModes; c2 < nmm; ++c2)
+                v[kk] = r < p.R ? float(double(v[kk]) * p.mfac[st][mm[c2]][p.g.coord(row, mm[c2]) * p.R + r]) : 0.f;
+            }
+          }
+          uint32_t h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) bf16_split_pair_fast(v[2 * e], v[2 * e + 1], h[e], l[e]);
+          hv[it] = make_uint4(h[0], h[1], h[2], h[3]);
+          lv[it] = make_uint4(l[0], l[1], l[2], l[3]);
+        }
+        if (gm > 0) tc::arrive(&g_empty[gs]);
+        tq = p.trace ? clock64() : 0;
+        tc::wait(&empty[slot], ((q / unsigned(L.nst)) & 1u) ^ 1u);
+        if (p.trace) { bw1 += clock64() - tq; }
+#pragma unroll
+        for (int it = 0; it < kMaxItems; ++it) {
+          const int i = tid + it * 128;
+          if (i >= nitems) break;
+          const int r = i % N, kg = (i / N) & 1, st = i / (2 * N);
+          const uint32_t off = uint32_t(r / 8) * kTcBSbo + uint32_t(kg) * 128 + uint32_t(r % 8) * 16;
+          const uint32_t tile = btiles + uint32_t((slot * 2 + st) * 2) * L.b_tile;
+          tc::sts_v4(tile + off, hv[it]);
+          tc::sts_v4(tile + L.b_tile + off, lv[it]);
         }
         tc::fence_proxy_async();
         tc::arrive(&b_full[slot]);
-        if (jb + kTcRows < j1) gather(jb + kTcRows + k, j1, itgt);
       }
+    }
+    if (p.trace && tid == 0) {
+      p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 0] = bw0;
+      p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 1] = bw1;
+      p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 2] = clock64() - b00;
     }
   } else {
     // ================= epilogue (warps 4..7: TMEM lane quarter = warp % 4) =================
@@ -383,13 +510,27 @@ static __global__ void __launch_bounds__(320, 1)
   if (warp == 9) tc::tmem_dealloc(tmem, uint32_t(p.tmem_cols));
 }
 
-// [K][R] fp64 -> [K][N] fp32 zero padded, for the case-B epilogue's 16-byte loads
-static __global__ void pad_last_kernel(const double* src, int64_t K, int R, int N, float* dst) {
-  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i >= K * N) return;
-  const int64_t k = i / N;
-  const int r = int(i % N);
-  dst[i] = r < R ? float(src[k * R + r]) : 0.f;
+// every factor of every stream, [I_m][R] fp64 -> [I_m][N] fp32 zero padded:
+// the B-operand gathers and the case-B epilogue's last factor (16-byte loads)
+struct F32Stage {
+  const double* src[2][kMaxOrder];
+  float* dst[2][kMaxOrder];
+  int64_t off[kMaxOrder + 1];  // cumulative I_m * N
+  int order, ns, R, N;
+};
+static __global__ void stage_f32_kernel(const F32Stage a) {
+  const int64_t tot = a.off[a.order];
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < tot * a.ns;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int s = int(i / tot);
+    const int64_t e = i - s * tot;
+    int m = 0;
+    while (e >= a.off[m + 1]) ++m;
+    const int64_t l = e - a.off[m];
+    const int64_t row = l / a.N;
+    const int r = int(l - row * a.N);
+    a.dst[s][m][l] = r < a.R ? float(a.src[s][m][row * a.R + r]) : 0.f;
+  }
 }
 
 // host P~/Q~ (fp64) -> bf16 hi/lo planes (step-level uploads).  The split is

@@ -13,9 +13,16 @@ if len(sys.argv) > 2:  # child
     import bench
     import paper_2602_14683_b200 as ntf
     beta = float(sys.argv[1])
-    x, init = bench.make_problem(bench.DIMS, bench.RANK, 0, 0, bench.DIMS[0], torch.device("cuda", 0))
-    cfg = ntf.FitConfig(beta=beta, rank=bench.RANK, inner_steps=bench.INNER, max_iters=3, precision="f32",
-                        use_graphs=False)
+    if os.environ.get("WORKLOAD") == "c5":  # 4-way CP, R = 64 (C5 shape; dim from C5_DIM, default 256)
+        from paper_2602_14683_b200 import io as nio
+        d = int(os.environ.get("C5_DIM", "256"))
+        x = nio.generate_cp_gamma((d,) * 4, 64, seed=0)
+        init = nio.cp_factors((d,) * 4, 64, seed=1, which="init")
+        cfg = ntf.FitConfig(beta=beta, rank=64, inner_steps=5, max_iters=1, precision="f32", use_graphs=False)
+    else:
+        x, init = bench.make_problem(bench.DIMS, bench.RANK, 0, 0, bench.DIMS[0], torch.device("cuda", 0))
+        cfg = ntf.FitConfig(beta=beta, rank=bench.RANK, inner_steps=bench.INNER, max_iters=3, precision="f32",
+                            use_graphs=False)
     ctx = ntf.default_context()
     ctx.set_profiling(True)
     try:

@@ -7,13 +7,15 @@ import sys
 launches, cur = [], None
 for line in open(sys.argv[1]):
     if line.startswith("launch"):
-        cur = [line.strip(), []]
+        cur = [line.strip(), [], []]
         launches.append(cur)
+    elif line.startswith("wstats"):
+        cur[2].append([int(x) for x in line.split()[1:]])
     else:
         v = [int(x) for x in line.split()]
         if v[5]:  # MMA side recorded
             cur[1].append(v)
-for hdr, rows in launches[:6]:
+for hdr, rows, ws in launches[:6]:
     if not rows:
         continue
     mma = [r[9] - r[5] for r in rows]           # unit MMA span (after acc_empty -> last commit)
@@ -26,3 +28,7 @@ for hdr, rows in launches[:6]:
     print(hdr)
     print("  unit MMA span %d  wait acc_empty %d  wait a_full %d  wait b_full %d  epilogue %d  commit->epi %d"
           % (med(mma), med(wait_empty), med(wa), med(wb), med(epi), med(epi_lag)))
+    if ws:
+        m = [med([w[i] for w in ws]) for i in range(7)]
+        print("  B: wait g_full %d wait empty %d total %d | gather: wait g_empty %d total %d | TMA: wait empty %d total %d"
+              % tuple(m))
