@@ -239,20 +239,30 @@ struct ColsumParams {
   double* out;
 };
 
+// column sums of every factor but `skip`, one block per mode: thread t sums
+// column t % R over the rows i = g, g + G, ... (g = t / R, G = 256 / R row
+// groups, coalesced across r), then column r adds its G group sums in group
+// order -- a fixed order, so results are reproducible (and identical on
+// every rank of a sharded fit).
 static __global__ void colsum_kernel(const ColsumParams p) {
   __shared__ double red[256];
   const int m = blockIdx.x;
   if (m == p.skip) return;
-  for (int r = 0; r < p.R; ++r) {
+  const int R = p.R, t = threadIdx.x;
+  for (int r0 = 0; r0 < R; r0 += 256) {
+    const int RC = R - r0 < 256 ? R - r0 : 256;
+    const int G = 256 / RC;
+    const int r = r0 + t % RC, g = t / RC;
     double s = 0.0;
-    for (int64_t i = threadIdx.x; i < p.rows[m]; i += blockDim.x) s += p.fac[m][i * p.R + r];
-    red[threadIdx.x] = s;
+    if (g < G)
+      for (int64_t i = g; i < p.rows[m]; i += G) s += p.fac[m][i * R + r];
+    red[t] = s;
     __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-      if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
-      __syncthreads();
+    if (t < RC) {
+      double tot = 0.0;
+      for (int q = 0; q < G; ++q) tot += red[q * RC + t];
+      p.out[m * R + r0 + t] = tot;
     }
-    if (threadIdx.x == 0) p.out[m * p.R + r] = red[0];
     __syncthreads();
   }
 }
