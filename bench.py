@@ -221,7 +221,80 @@ def run_ours(args, rank_id, world, local_rank):
         del xh
 
     c4 = run_c4(args, ctx, dev) if world == 1 and args.c4 else None
-    return per_beta, launches, pst, clocks, e2e, c4
+    c5 = run_c5(args, rank_id, world, local_rank, dev, dist, max_over_ranks) if args.c5 else None
+    return per_beta, launches, pst, clocks, e2e, c4, c5
+
+
+C5_DIM = 256
+C5_RANK = 64
+C5_INNER = 5
+C5_BETA = 0.5
+
+
+def run_c5(args, rank_id, world, local_rank, dev, dist, max_over_ranks):
+    """C5 (BASELINE configs[4]): dense 4-way CP 256^4 fp32 (17 GB), R=64,
+    beta=0.5, J-CoMM L=5.  Mode-0 slabs generated in place on each rank
+    (Philox, paper_2602_14683_b200.io); factors replicated, Num/Den partials
+    allreduced.  value = outer iterations / device time (max over ranks) of
+    C5_STEPS timed outer iterations after one warm-up."""
+    import torch
+    import paper_2602_14683_b200 as ntf
+    from paper_2602_14683_b200 import io as nio
+    dims = (C5_DIM,) * 4
+    row0 = C5_DIM * rank_id // world
+    row1 = C5_DIM * (rank_id + 1) // world
+    x = nio.generate_cp_gamma(dims, C5_RANK, seed=0, rows=(row0, row1), device=local_rank)
+    init = nio.cp_factors(dims, C5_RANK, seed=1, which="init")
+    init[0] = init[0][row0:row1].copy()
+    ctx = ntf.Context(local_rank)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+    shard = None
+    if world > 1:
+        comm = torch.zeros(2 * C5_DIM * C5_RANK + 8, dtype=torch.float64, device=dev)
+        ctx.set_comm_buffer(comm.data_ptr(), comm.numel())
+
+        def allreduce(ptr, count, strm):
+            with torch.cuda.stream(stream):
+                dist.all_reduce(comm[:count])
+
+        ctx.set_allreduce(allreduce)
+        shard = (C5_DIM, row0)
+    steps = max(1, min(args.c5_steps, args.steps))
+    cfg = lambda it: ntf.FitConfig(beta=C5_BETA, rank=C5_RANK, inner_steps=C5_INNER, max_iters=it, precision="f32")
+    with torch.cuda.stream(stream):
+        ntf.jcomm_fit(x, init, cfg(1), ctx=ctx, shard=shard)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        res = ntf.jcomm_fit(x, init, cfg(steps), ctx=ctx, shard=shard)
+        torch.cuda.synchronize()
+    ms = max_over_ranks(ctx.stats()["device_ms"]) / steps
+    launches = ctx.stats()["kernel_launches"]
+    ctx.set_profiling(True)
+    with torch.cuda.stream(stream):
+        ntf.jcomm_fit(x, init, cfg(1), ctx=ctx, shard=shard)
+    pst = ctx.stats()
+    ctx.set_profiling(False)
+    E = C5_DIM ** 4
+    alg = 4.0 * E * (1 + 2 + 2 * C5_INNER * 4)  # X + P~,Q~ written once, read once per inner block update
+    k3_ms = pst["contract_ms"] / max(1, pst["contract_launches"])
+    k3_bytes = 8.0 * E / world
+    peak, peak_src = peaks()
+    out = {"workload": "C5: dense CP 256^4 fp32 (17 GB), R=64, beta=0.5, J-CoMM L=5, mode-0 slabs "
+                       f"dp{world}", "outer_it_per_s": 1e3 / ms, "ms_per_step": ms, "steps": steps,
+           "final_loss": res.trace[-1].loss, "gpu_launches": launches,
+           "alg_bytes_per_outer": alg, "alg_GBps_whole_step": alg / (ms * 1e-3) / 1e9,
+           "roofline_k3": {"bound": "hbm", "kernel": "tc_contract_kernel<64>", "achieved": k3_bytes / (k3_ms * 1e-3) / 1e9,
+                           "peak": peak, "unit": "GB/s", "frac": k3_bytes / (k3_ms * 1e-3) / 1e9 / peak,
+                           "peak_source": peak_src, "avg_launch_ms": k3_ms,
+                           "algorithmic_bytes_per_launch": k3_bytes},
+           "kernel_breakdown_ms_per_step": {"recon": pst["recon_ms"], "contract": pst["contract_ms"],
+                                            "other": pst["device_ms"] - pst["recon_ms"] - pst["contract_ms"]}}
+    del x
+    ctx.trim()
+    torch.cuda.empty_cache()
+    return out
 
 
 C4_DIMS = (183, 24, 1140, 1717)
@@ -350,6 +423,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-c4", dest="c4", action="store_false", help="skip the sparse C4 side measurement")
+    ap.add_argument("--no-c5", dest="c5", action="store_false", help="skip the large dense C5 side measurement")
+    ap.add_argument("--c5-steps", type=int, default=2, help="timed C5 outer iterations (each ~0.2 s on one B200)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -367,7 +442,7 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
-    per_beta, launches, pst, clocks, e2e, c4 = run_ours(args, rank_id, world, local_rank)
+    per_beta, launches, pst, clocks, e2e, c4, c5 = run_ours(args, rank_id, world, local_rank)
 
     if rank_id == 0:
         E = int(np.prod(DIMS))
@@ -404,6 +479,7 @@ def main():
                          "algorithmic_bytes_per_launch": ebytes, "avg_launch_ms": avg_ms,
                          "fma_rate_tflops_equiv": fma_rate, "fma_frac": fma_rate / FFMA_PEAK_T},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "c4_sparse": c4,
+            "c5_large": c5,
             "kernel_breakdown_ms_per_step": {
                 "recon": pst["recon_ms"] / max(1, min(args.steps, 5)),
                 "contract": pst["contract_ms"] / max(1, min(args.steps, 5)),

@@ -646,7 +646,7 @@ class CpEngine {
       p.fac[m] = fac[m];
     }
     p.out = colsum_;
-    colsum_kernel<<<N_, 256, 0, c_.stream>>>(p);
+    colsum_kernel<<<N_, kColsumThreads, 0, c_.stream>>>(p);
     NTFG_LAUNCHED(c_);
     if (sharded_ && skip != 0) allreduce(colsum_, size_t(R_));  // slab-local mode-0 colsum
     colprod_kernel<<<int(ceil_div(R_, 64)), 64, 0, c_.stream>>>(colsum_, N_, skip, int(R_), colprod_);

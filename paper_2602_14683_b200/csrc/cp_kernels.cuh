@@ -239,24 +239,36 @@ struct ColsumParams {
   double* out;
 };
 
-// column sums of every factor but `skip`, one block per mode: thread t sums
-// column t % R over the rows i = g, g + G, ... (g = t / R, G = 256 / R row
-// groups, coalesced across r), then column r adds its G group sums in group
-// order -- a fixed order, so results are reproducible (and identical on
-// every rank of a sharded fit).
-static __global__ void colsum_kernel(const ColsumParams p) {
-  __shared__ double red[256];
+// column sums of every factor but `skip`, one 1024-thread block per mode:
+// thread t sums column t % RC over the rows i = g, g + G, ... (g = t / RC,
+// G = 1024 / RC row groups, coalesced across r) into four interleaved
+// partials (four loads in flight), then column r adds its G group sums in
+// group order -- a fixed order, so results are reproducible (and identical
+// on every rank of a sharded fit).
+constexpr int kColsumThreads = 1024;
+static __global__ void __launch_bounds__(kColsumThreads) colsum_kernel(const ColsumParams p) {
+  __shared__ double red[kColsumThreads];
   const int m = blockIdx.x;
   if (m == p.skip) return;
   const int R = p.R, t = threadIdx.x;
-  for (int r0 = 0; r0 < R; r0 += 256) {
-    const int RC = R - r0 < 256 ? R - r0 : 256;
-    const int G = 256 / RC;
+  const int64_t rows = p.rows[m];
+  for (int r0 = 0; r0 < R; r0 += kColsumThreads) {
+    const int RC = R - r0 < kColsumThreads ? R - r0 : kColsumThreads;
+    const int G = kColsumThreads / RC;
     const int r = r0 + t % RC, g = t / RC;
-    double s = 0.0;
-    if (g < G)
-      for (int64_t i = g; i < p.rows[m]; i += G) s += p.fac[m][i * R + r];
-    red[t] = s;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (g < G) {
+      const double* f = p.fac[m] + r;
+      int64_t i = g;
+      for (; i + 3 * int64_t(G) < rows; i += 4 * int64_t(G)) {
+        s0 += f[i * R];
+        s1 += f[(i + G) * R];
+        s2 += f[(i + 2 * G) * R];
+        s3 += f[(i + 3 * G) * R];
+      }
+      for (; i < rows; i += G) s0 += f[i * R];
+    }
+    red[t] = (s0 + s1) + (s2 + s3);
     __syncthreads();
     if (t < RC) {
       double tot = 0.0;
@@ -308,12 +320,23 @@ static __global__ void objective_finalize_kernel(const double* partials, int n, 
 // deterministic): sum x^b / (b (b-1)), for the tensor-core recon's split
 // objective (stream3_kernels.cuh, tc_weights).  Two stages: per-CTA partials
 // then one CTA.
+// x^beta of one data entry: fp32 data with beta = 0.5 / 1.5 uses the
+// correctly rounded sqrtf (unbiased, ~6e-8 relative; the fp64 pow is ~40 fp64
+// instructions per entry and made this pass compute-bound)
+template <typename T>
+__device__ __forceinline__ double xpow_term(T x, double beta) {
+  if constexpr (sizeof(T) == 4) {
+    if (beta == 0.5) return double(sqrtf(x));
+    if (beta == 1.5) return double(x) * double(sqrtf(x));
+  }
+  return fpow64(double(x), beta);
+}
 template <typename T>
 static __global__ void xconst_kernel(const T* x, int64_t n, double beta, double* partials) {
   __shared__ double red[256];
   double s = 0.0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-    s += fpow64(double(x[i]), beta);
+    s += xpow_term(x[i], beta);
   red[threadIdx.x] = s;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
