@@ -356,7 +356,7 @@ class CpEngine {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemMax)),
                    "cudaFuncSetAttribute");
     }
-    kern<<<grid, 352, p.lay.total, c_.stream>>>(maps, p);
+    kern<<<grid, p.N <= 32 ? tc_threads<32>() : tc_threads<64>(), p.lay.total, c_.stream>>>(maps, p);
     NTFG_LAUNCHED(c_);
   }
   bool tc() const { return tc_; }

@@ -14,7 +14,7 @@
 //
 // Warp roles (352 threads): 0-3 build the B tiles (M rows), 4-7 epilogue
 // (tcgen05.ld -> partials), 8 TMA producer, 9 TMEM allocator + single-thread
-// MMA issuer, 10 factor-row gathers.  Stages of 16 rows cycle through a smem ring (2-6 deep, sized
+// MMA issuer (+ warp 11: second issuer), 10 factor-row gathers.  Stages of 16 rows cycle through a smem ring (2-6 deep, sized
 // from K at launch) guarded by mbarriers (TMA tx, B-tile arrivals,
 // tcgen05.commit); the TMEM accumulator is double-buffered across units when
 // it fits so the epilogue of one unit overlaps the next.
@@ -42,6 +42,11 @@ namespace ntfg {
 constexpr int kTcRows = 16;     // UMMA K for 16-bit inputs
 constexpr int kTcMaxStages = 6;
 constexpr int kTcMaxGather = 6;
+// MMA-issuing warps (9, and 11 when 2): one issuing thread was the stage-rate
+// limit at N <= 32 (C2 K3 0.198 -> 0.189 ms); at N = 64 a second issuer gains
+// nothing and its registers push the kernel into spills, so it stays at one
+template <int N> __host__ __device__ constexpr int tc_issuers() { return N <= 32 ? 2 : 1; }
+template <int N> __host__ __device__ constexpr int tc_threads() { return 352 + 32 * (tc_issuers<N>() - 1); }
 constexpr int kTcBSbo = 272;    // bytes between 8-column groups of a B tile (256 + 16: bank spread)
 constexpr int kTcGModes = 3;    // factor modes gathered through the cp.async ring (more: direct fp64)
 constexpr size_t kTcSmemMax = 227 * 1024 - 2560;  // dynamic budget (static smem 2.3 KB)
@@ -95,7 +100,7 @@ __device__ __forceinline__ void bf16_split(double v, __nv_bfloat16& hi, __nv_bfl
 }
 
 template <int NMAX>
-static __global__ void __launch_bounds__(352, 1)
+static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     tc_contract_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   const TcLayout& L = p.lay;
   extern __shared__ unsigned char smem_raw[];
@@ -114,14 +119,14 @@ static __global__ void __launch_bounds__(352, 1)
     for (int s = 0; s < L.nst; ++s) {
       tc::mbar_init(&a_full[s], 1);
       tc::mbar_init(&b_full[s], 128);
-      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&empty[s], tc_issuers<NMAX>());
     }
     for (int g = 0; g < L.gdepth; ++g) {
       tc::mbar_init(&g_full[g], 1);
       tc::mbar_init(&g_empty[g], 128);
     }
     for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_full[b], tc_issuers<NMAX>());
       tc::mbar_init(&acc_empty[b], 128);
     }
   }
@@ -196,8 +201,12 @@ static __global__ void __launch_bounds__(352, 1)
         p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 6] = clock64() - t00;
       }
     }
-  } else if (warp == 9) {
-    // ================= MMA issuer =================
+  } else if (warp == 9 || (warp == 11 && tc_issuers<NMAX>() > 1)) {
+    // ================= MMA issuers =================
+    // issuer i (warp 9: 0, warp 11: 1) owns the accumulator tiles (s, m) with
+    // (s * mt + m) % 2 == i; each commits every stage slot and unit buffer
+    // (barrier counts kTcIssuers)
+    const int issuer = warp == 9 ? 0 : 1;
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_bf16_f32(128, N, true, false);
       uint32_t q = 0, it = 0;
@@ -206,7 +215,7 @@ static __global__ void __launch_bounds__(352, 1)
         unit_range(u, j0, j1, itgt, split);
         const uint32_t tb = p.dbuf ? (it & 1u) : 0u;
         const uint32_t use = p.dbuf ? (it >> 1) : it;  // uses of this accumulator buffer so far
-        unsigned long long* tr = (p.trace && it < 16) ? p.trace + (size_t(blockIdx.x) * 16 + it) * 8 : nullptr;
+        unsigned long long* tr = (p.trace && it < 16 && issuer == 0) ? p.trace + (size_t(blockIdx.x) * 16 + it) * 8 : nullptr;
         if (tr) tr[2] = clock64();
         tc::wait(&acc_empty[tb], (use & 1u) ^ 1u);
         tc::fence_after_sync();
@@ -229,6 +238,7 @@ static __global__ void __launch_bounds__(352, 1)
             const uint64_t bh = tc::desc_k_interleave(stage_b(slot, s, 0), 128, kTcBSbo);
             const uint64_t bl = tc::desc_k_interleave(stage_b(slot, s, 1), 128, kTcBSbo);
             for (int m = 0; m < p.mt; ++m) {
+              if (((s * p.mt + m) % tc_issuers<NMAX>()) != issuer) continue;
               const uint32_t d = tmem + tb * uint32_t(cols_per_buf) + uint32_t((s * p.mt + m) * N);
               const uint64_t ah = tc::desc_mn_sw128(stage_a(slot, s, 0) + size_t(m) * 4096, 2048, 1024);
               const uint64_t al = tc::desc_mn_sw128(stage_a(slot, s, 1) + size_t(m) * 4096, 2048, 1024);
