@@ -221,7 +221,12 @@ def run_ours(args, rank_id, world, local_rank):
         del xh
 
     c4 = run_c4(args, ctx, dev) if world == 1 and args.c4 else None
-    c5 = run_c5(args, rank_id, world, local_rank, dev, dist, max_over_ranks) if args.c5 else None
+    c5 = None
+    if args.c5:
+        try:  # a side measurement must never sink the headline line
+            c5 = run_c5(args, rank_id, world, local_rank, dev, dist, max_over_ranks)
+        except Exception as ex:
+            c5 = {"workload": "C5", "error": f"{type(ex).__name__}: {str(ex)[:200]}"}
     return per_beta, launches, pst, clocks, e2e, c4, c5
 
 
@@ -289,8 +294,8 @@ def run_c5(args, rank_id, world, local_rank, dev, dist, max_over_ranks):
                            "peak": peak, "unit": "GB/s", "frac": k3_bytes / (k3_ms * 1e-3) / 1e9 / peak,
                            "peak_source": peak_src, "avg_launch_ms": k3_ms,
                            "algorithmic_bytes_per_launch": k3_bytes},
-           "kernel_breakdown_ms_per_step": {"recon": pst["recon_ms"], "contract": pst["contract_ms"],
-                                            "other": pst["device_ms"] - pst["recon_ms"] - pst["contract_ms"]}}
+           "kernel_ms_one_profiled_outer": {"recon": pst["recon_ms"], "contract": pst["contract_ms"],
+                                            "note": "eager launches bracketed by events; includes the fit's final objective pass"}}
     del x
     ctx.trim()
     torch.cuda.empty_cache()
