@@ -437,8 +437,8 @@ class CpEngine {
       for (int m = 0; m < N_ - 1; ++m)
         if (m != n) f = m;
       p.gfast = (f >= 0 && g_.dims[f] % kTcRows == 0) ? 1 : 0;
-      static const bool slow = [] { const char* e = std::getenv("NTFG_TC_SLOW_GATHER"); return e && e[0] == '1'; }();
-      if (slow) p.gfast = 0;
+      const char* slow = std::getenv("NTFG_TC_SLOW_GATHER");  // tests: force the per-row gather path
+      if (slow && slow[0] == '1') p.gfast = 0;
     }
     p.partA = reinterpret_cast<float*>(partA_);
     p.partB = partB_;

@@ -75,3 +75,29 @@ def test_tc_reference_planes_round_trip():
     got = ntf.jcomm_inner_update(cur, ctx, 1, 0.5, EPS, precision="f32")
     want = O.jcomm_inner_update(cur, (f, op, oq), 1, 0.5, EPS)
     assert relm(got, want) < 1e-4
+
+
+# Shapes that take the fast paths added with the gather warp and the tile
+# reconstruction: every off-mode block of 16 rows contiguous (gfast) and
+# 32 | I_f for the tile recon's G * A_f rows (NPRE 2 and 3), R > 32
+# (N = 64, RP = 64), and a 4-way tensor whose modes are all fast.
+@pytest.mark.parametrize("beta", [0.5, 1.0])
+@pytest.mark.parametrize("dims,rank", [((4, 16, 32, 128), 64), ((16, 64, 128), 40), ((32, 32, 256), 17)])
+def test_tc_fast_paths_match_oracle(beta, dims, rank):
+    x, init = problem(dims, rank, 11)
+    cfg = ntf.FitConfig(beta=beta, rank=rank, max_iters=8, inner_steps=2, precision="f32")
+    res = ntf.jcomm_fit(x, init, cfg)
+    om, otr = O.jcomm_fit(x, init, O.FitConfig(beta=beta, rank=rank, max_iters=8, inner_steps=2))
+    assert relm(res.model, om) < 1e-4
+    assert O.rel_err([t.loss for t in res.trace], [t[2] for t in otr]) < 1e-5
+
+
+@pytest.mark.parametrize("dims", [(4, 16, 32, 128), (16, 64, 128)])
+def test_tc_fast_and_generic_gathers_agree(dims, monkeypatch):
+    # NTFG_TC_SLOW_GATHER=1 forces the per-row gather path: same products, same order
+    x, init = problem(dims, 24, 13)
+    cfg = ntf.FitConfig(beta=0.5, rank=24, max_iters=4, inner_steps=2, precision="f32")
+    a = ntf.jcomm_fit(x, init, cfg)
+    monkeypatch.setenv("NTFG_TC_SLOW_GATHER", "1")
+    b = ntf.jcomm_fit(x, init, cfg)
+    assert all(np.array_equal(u, v) for u, v in zip(a.model, b.model))
