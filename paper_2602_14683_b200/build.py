@@ -3,6 +3,7 @@
   libntfg.so      C ABI + CUDA kernels (include/ntfg.h)
   libntf_b200.so  drop-in C++ API, namespace ntf (include/ntf/ntf.hpp),
                   a thin layer over libntfg.so
+  ntf-cli         the reference's command-line front end over libntf_b200
 
 Both land in paper_2602_14683_b200/lib/ (git-ignored, shipped to the GPU box
 with the repo snapshot).  Objects are rebuilt only when a source or header is
@@ -77,6 +78,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if force or _stale(lib2, api_srcs + hdrs + [lib]):
             _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I" + INCLUDE, "-o", lib2] + api_srcs
                  + ["-L" + LIB, "-lntfg", "-Wl,-rpath,$ORIGIN"])
+        # reference CLI front end (tools/ntf_main.cpp) over the drop-in library
+        cli_src = os.path.join(CSRC, "ntf_cli.cpp")
+        cli = os.path.join(LIB, "ntf-cli")
+        if os.path.exists(cli_src) and (force or _stale(cli, [cli_src, lib2] + hdrs)):
+            _run(["g++", "-std=c++20", "-O2", "-I" + INCLUDE, "-o", cli, cli_src, "-L" + LIB, "-lntf_b200", "-lntfg",
+                  "-Wl,-rpath,$ORIGIN"])
     return lib
 
 

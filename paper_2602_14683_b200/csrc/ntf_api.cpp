@@ -3,6 +3,8 @@
 // (/root/reference/proj/src/{tensor,cp,tucker,divergence,config}.cpp);
 // every E-sized computation runs on the GPU through ntfg_*.
 #include "ntf/ntf.hpp"
+#include "ntf/io.hpp"
+#include "ntf/unfold.hpp"
 
 #include <cmath>
 #include <cstring>
@@ -528,6 +530,248 @@ TuckerFitResult tucker_bcomm_fit(const DenseTensor& x, TuckerModel init, const F
 
 TuckerFitResult tucker_jcomm_fit(const DenseTensor& x, TuckerModel init, const FitConfig& cfg) {
     return tucker_fit(NTFG_JCOMM, x, std::move(init), cfg);
+}
+
+// ---- io.hpp (reference io.cpp): CTF1 / COO / trace through the C ABI ----------------
+
+void write_tensor(const std::string& path, const DenseTensor& t) {
+    const auto dims = u64(t.shape());
+    ok(ntfg_ctf1_write(nullptr, path.c_str(), std::uint32_t(dims.size()), dims.data(), t.data(), 0, NTFG_HOST));
+}
+
+DenseTensor read_tensor(const std::string& path, std::size_t max_entries) {
+    std::uint32_t order = 0;
+    std::uint64_t dims[256];
+    ok(ntfg_ctf1_header(path.c_str(), &order, dims, 256, max_entries));
+    DenseTensor t(std::vector<std::size_t>(dims, dims + order));
+    ok(ntfg_ctf1_read(nullptr, path.c_str(), t.data(), 0, NTFG_HOST, max_entries));
+    return t;
+}
+
+DenseTensor cwise_max(const DenseTensor& a, double s) {
+    DenseTensor out = a;
+    for (double& v : out.values()) v = std::max(v, s);
+    return out;
+}
+
+DenseTensor read_coo(const std::string& path, std::optional<double> floor, std::size_t max_entries) {
+    std::uint32_t order = 0;
+    std::uint64_t dims[256];
+    std::uint64_t nnz = 0;
+    ok(ntfg_coo_text_read(path.c_str(), &order, dims, 256, &nnz, nullptr, nullptr, 0, max_entries));
+    std::vector<std::int32_t> idx(std::max<std::uint64_t>(nnz, 1) * order);
+    std::vector<double> vals(std::max<std::uint64_t>(nnz, 1));
+    ok(ntfg_coo_text_read(path.c_str(), &order, dims, 256, &nnz, idx.data(), vals.data(), nnz, max_entries));
+    DenseTensor t(std::vector<std::size_t>(dims, dims + order));
+    for (std::uint64_t e = 0; e < nnz; ++e) {  // duplicates accumulate in input order (io.cpp:138)
+        std::size_t flat = 0;
+        for (std::uint32_t m = 0; m < order; ++m) flat = flat * dims[m] + std::size_t(idx[e * order + m]);
+        t[flat] += vals[e];
+    }
+    if (floor) return cwise_max(t, *floor);
+    return t;
+}
+
+DenseTensor read_tensor_auto(const std::string& path, std::size_t max_entries) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw FormatError("cannot open: " + path);
+    char head[4] = {};
+    const std::size_t got = std::fread(head, 1, 4, f);
+    std::fclose(f);
+    if (got == 4 && std::memcmp(head, "CTF1", 4) == 0) return read_tensor(path, max_entries);
+    return read_coo(path, std::nullopt, max_entries);
+}
+
+void write_trace(const std::string& path, std::span<const TraceRecord> records) {
+    std::vector<ntfg_trace_row> rows(records.size());
+    for (std::size_t i = 0; i < records.size(); ++i) rows[i] = {records[i].iter, records[i].time_s, records[i].loss};
+    ok(ntfg_trace_write(path.c_str(), rows.data(), rows.size()));
+}
+
+std::vector<TraceRecord> read_trace(const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) throw FormatError("cannot open: " + path);
+    std::vector<TraceRecord> out;
+    char line[512];
+    std::size_t lineno = 0;
+    while (std::fgets(line, sizeof line, f)) {
+        ++lineno;
+        if (lineno == 1) {
+            if (std::strncmp(line, "iter,time_s,loss", 16) != 0) {
+                std::fclose(f);
+                throw ParseError("trace header must be iter,time_s,loss", lineno);
+            }
+            continue;
+        }
+        unsigned long long it = 0;
+        double t = 0.0, l = 0.0;
+        if (std::sscanf(line, "%llu,%lf,%lf", &it, &t, &l) != 3) {
+            std::fclose(f);
+            throw ParseError("malformed trace row", lineno);
+        }
+        out.push_back({std::size_t(it), t, l});
+    }
+    std::fclose(f);
+    return out;
+}
+
+// the reference generator: std::mt19937_64 seeded with seed_seq{seed lo, seed hi,
+// stream lo, stream hi}; uniform01 keeps the top 53 bits (io.cpp:190-200)
+Rng::Rng(std::uint64_t seed, std::uint64_t stream) {
+    std::seed_seq seq{std::uint32_t(seed & 0xffffffffu), std::uint32_t(seed >> 32), std::uint32_t(stream & 0xffffffffu),
+                      std::uint32_t(stream >> 32)};
+    engine_.seed(seq);
+}
+
+double Rng::uniform01() { return double(engine_() >> 11) * 0x1.0p-53; }
+
+static Matrix random_matrix(std::size_t rows, std::size_t cols, Rng& rng, double eps) {
+    Matrix m(rows, cols);
+    for (double& v : m.values()) v = std::max(rng.uniform01(), eps);
+    return m;
+}
+
+CpFactors random_cp_factors(std::span<const std::size_t> dims, std::size_t rank, Rng& rng, double eps) {
+    std::vector<Matrix> f;
+    for (std::size_t d : dims) f.push_back(random_matrix(d, rank, rng, eps));
+    return CpFactors(std::move(f));
+}
+
+TuckerModel random_tucker_model(std::span<const std::size_t> dims, std::span<const std::size_t> ranks, Rng& rng,
+                                double eps) {
+    if (dims.size() != ranks.size()) throw ShapeError("random_tucker_model: dims and ranks length mismatch");
+    DenseTensor core(std::vector<std::size_t>(ranks.begin(), ranks.end()));
+    for (double& v : core.values()) v = std::max(rng.uniform01(), eps);
+    std::vector<Matrix> f;
+    for (std::size_t n = 0; n < dims.size(); ++n) f.push_back(random_matrix(dims[n], ranks[n], rng, eps));
+    return TuckerModel(std::move(core), std::move(f));
+}
+
+CpFactors init_cp_factors(std::span<const std::size_t> dims, std::size_t rank, std::uint64_t seed, double eps) {
+    Rng rng(seed, Rng::kInitStream);
+    return random_cp_factors(dims, rank, rng, eps);
+}
+
+TuckerModel init_tucker_model(std::span<const std::size_t> dims, std::span<const std::size_t> ranks,
+                              std::uint64_t seed, double eps) {
+    Rng rng(seed, Rng::kInitStream);
+    return random_tucker_model(dims, ranks, rng, eps);
+}
+
+std::pair<DenseTensor, CpFactors> synth_cp(std::span<const std::size_t> dims, std::size_t rank, std::uint64_t seed,
+                                           double eps) {
+    Rng rng(seed, Rng::kSynthStream);
+    CpFactors truth = random_cp_factors(dims, rank, rng, eps);
+    DenseTensor x = cp_reconstruct(truth);
+    return {std::move(x), std::move(truth)};
+}
+
+std::pair<DenseTensor, TuckerModel> synth_tucker(std::span<const std::size_t> dims,
+                                                 std::span<const std::size_t> ranks, std::uint64_t seed,
+                                                 double eps) {
+    Rng rng(seed, Rng::kSynthStream);
+    TuckerModel truth = random_tucker_model(dims, ranks, rng, eps);
+    DenseTensor x = tucker_reconstruct(truth);
+    return {std::move(x), std::move(truth)};
+}
+
+// ---- unfold.hpp (reference unfold.cpp) ---------------------------------------------
+
+static std::vector<std::size_t> unfold_strides(const std::vector<std::size_t>& shape, std::size_t mode) {
+    std::vector<std::size_t> st(shape.size(), 0);
+    std::size_t stride = 1;
+    for (std::size_t a = shape.size(); a-- > 0;) {  // remaining modes ascending, last fastest
+        if (a == mode) continue;
+        st[a] = stride;
+        stride *= shape[a];
+    }
+    return st;
+}
+
+UnfoldedView unfold(const DenseTensor& t, std::size_t mode) {
+    if (mode >= t.order()) throw ShapeError("unfold: mode out of range");
+    const std::size_t rows = t.shape()[mode];
+    const auto st = unfold_strides(t.shape(), mode);
+    Matrix m(rows, t.size() / rows);
+    MultiIndex idx(t.order(), 0);
+    std::size_t flat = 0;
+    do {
+        std::size_t c = 0;
+        for (std::size_t a = 0; a < t.order(); ++a)
+            if (a != mode) c += idx[a] * st[a];
+        m(idx[mode], c) = t[flat++];
+    } while (next_multi_index(idx, t.shape()));
+    return {std::move(m), mode};
+}
+
+DenseTensor refold(const UnfoldedView& u, std::span<const std::size_t> shape) {
+    if (u.mode >= shape.size()) throw ShapeError("refold: mode out of range");
+    DenseTensor t(std::vector<std::size_t>(shape.begin(), shape.end()));
+    if (u.matrix.rows() != t.shape()[u.mode] || u.matrix.size() != t.size())
+        throw ShapeError("refold: matrix does not match target shape");
+    const auto st = unfold_strides(t.shape(), u.mode);
+    MultiIndex idx(t.order(), 0);
+    std::size_t flat = 0;
+    do {
+        std::size_t c = 0;
+        for (std::size_t a = 0; a < t.order(); ++a)
+            if (a != u.mode) c += idx[a] * st[a];
+        t[flat++] = u.matrix(idx[u.mode], c);
+    } while (next_multi_index(idx, t.shape()));
+    return t;
+}
+
+Matrix khatri_rao(std::span<const Matrix> mats) {
+    if (mats.empty()) throw ShapeError("khatri_rao: at least one matrix required");
+    const std::size_t r = mats.front().cols();
+    for (const Matrix& m : mats)
+        if (m.cols() != r) throw ShapeError("khatri_rao: inconsistent column counts");
+    Matrix out = mats.front();
+    for (std::size_t k = 1; k < mats.size(); ++k) {
+        const Matrix& b = mats[k];
+        Matrix next(out.rows() * b.rows(), r);
+        for (std::size_t ia = 0; ia < out.rows(); ++ia)
+            for (std::size_t ib = 0; ib < b.rows(); ++ib)
+                for (std::size_t c = 0; c < r; ++c) next(ia * b.rows() + ib, c) = out(ia, c) * b(ib, c);
+        out = std::move(next);
+    }
+    return out;
+}
+
+CpFactors mu_unfold_cp_sweep(const CpFactors& f, const DenseTensor& x, const BetaParam& p, double eps) {
+    require_dims(f.factors, x, "mu_unfold_cp_sweep");
+    auto flat = concat(f.factors);
+    const auto dims = u64(x.shape());
+    ok(ntfg_cp_mu_unfold_sweep(ctx(), NTFG_F64, p.beta(), eps, std::uint32_t(dims.size()), dims.data(), x.data(),
+                               f.rank(), flat.data()));
+    CpFactors out = f;
+    split_into(flat, out.factors);
+    return out;
+}
+
+CpFitResult mu_unfold_cp_fit(const DenseTensor& x, CpFactors init, const FitConfig& cfg) {
+    validate_fit_config(cfg);
+    require_dims(init.factors, x, "mu_unfold_cp_fit");
+    std::vector<std::uint64_t> keep;
+    ntfg_fit_config c = to_c(cfg, keep);
+    c.rank = init.rank();
+    auto flat = concat(init.factors);
+    std::vector<ntfg_trace_row> rows(cfg.max_iters + 1);
+    std::uint64_t n = 0;
+    const auto dims = u64(x.shape());
+    ok(ntfg_cp_mu_unfold_fit(ctx(cfg.device), &c, std::uint32_t(dims.size()), dims.data(), x.data(), 0, NTFG_HOST,
+                             flat.data(), rows.data(), &n));
+    CpFitResult out{std::move(init), trace_of(rows, n)};
+    split_into(flat, out.model.factors);
+    return out;
+}
+
+TuckerModel mu_unfold_tucker_sweep(const TuckerModel&, const DenseTensor&, const BetaParam&, double) {
+    throw DomainError("mu_unfold_tucker_sweep: the Tucker MU-unfold baseline is not part of the B200 build");
+}
+
+TuckerFitResult mu_unfold_tucker_fit(const DenseTensor&, TuckerModel, const FitConfig&) {
+    throw DomainError("mu_unfold_tucker_fit: the Tucker MU-unfold baseline is not part of the B200 build");
 }
 
 }  // namespace ntf
