@@ -1078,7 +1078,7 @@ class CpEngine {
   void launch_tile_bk(const ReconParams<float>& p) {
     // fast H: 1..3 row modes, the fastest with 32 | I (tiles never straddle its blocks)
     const int npre = N_ - 1;
-    const bool fast = npre >= 1 && npre <= 3 && g_.dims[npre - 1] % kRtRows == 0;
+    const bool fast = npre >= 1 && npre <= 3 && g_.dims[npre - 1] % kRtRows == 0 && g_.small_rows;
     if (!fast) launch_tile_np<RP, BK, 0>(p);
     else if (npre == 1) launch_tile_np<RP, BK, 1>(p);
     else if (npre == 2) launch_tile_np<RP, BK, 2>(p);

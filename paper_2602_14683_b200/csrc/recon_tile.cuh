@@ -138,10 +138,24 @@ static __global__ void __launch_bounds__(kRtThreads, 2) recon_tile_kernel(const 
       return;
     }
     if constexpr (NPRE >= 1) {
+      // row0 -> (c_0, .., c_{NPRE-1}) with NPRE - 1 divisions (row < 2^31 on this path)
+      int64_t c[3] = {0, 0, 0};
+      int64_t q = row0;
+      if constexpr (NPRE == 3) {
+        const int64_t t = p.g.fd[2].div(q);
+        c[2] = q - t * p.g.dims[2];
+        c[0] = p.g.fd[1].div(t);
+        c[1] = t - c[0] * p.g.dims[1];
+      } else if constexpr (NPRE == 2) {
+        c[0] = p.g.fd[1].div(q);
+        c[1] = q - c[0] * p.g.dims[1];
+      } else {
+        c[0] = q;
+      }
       double g = 1.0;
-      if constexpr (NPRE >= 2) g = p.fac[0][p.g.coord(row0, 0) * R + hr];
-      if constexpr (NPRE >= 3) g *= p.fac[1][p.g.coord(row0, 1) * R + hr];
-      const double* fr = p.fac[NPRE - 1] + (p.g.coord(row0, NPRE - 1) + hrr0) * R + hr;
+      if constexpr (NPRE >= 2) g = p.fac[0][c[0] * R + hr];
+      if constexpr (NPRE >= 3) g *= p.fac[1][c[1] * R + hr];
+      const double* fr = p.fac[NPRE - 1] + (c[NPRE - 1] + hrr0) * R + hr;
 #pragma unroll
       for (int it = 0; it < HI; ++it) {
         const double v = fr[int64_t(it) * (kRtThreads / RP) * R];
@@ -168,12 +182,16 @@ static __global__ void __launch_bounds__(kRtThreads, 2) recon_tile_kernel(const 
     for (int it = 0; it < HI; ++it) hs[(size_t(buf) * RP + hr) * HS + hrr0 + it * (kRtThreads / RP)] = hv[it];
   };
   auto load_x = [&](int64_t tile, float4 (&xv)[4]) {
-    const float* xb = p.x + (tile * kRtRows + warp * 4) * K + kcol;
+    const int64_t row = tile * kRtRows + warp * 4;
+    const float* xb = p.x + row * K + kcol;
+    if (row + 4 <= rows) {  // every row of a full tile (tile < ntiles implied)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t row = tile * kRtRows + warp * 4 + i;
-      xv[i] = (tile < ntiles && row < rows) ? __ldg(reinterpret_cast<const float4*>(xb + i * K))
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < 4; ++i) xv[i] = __ldg(reinterpret_cast<const float4*>(xb + i * K));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        xv[i] = (tile < ntiles && row + i < rows) ? __ldg(reinterpret_cast<const float4*>(xb + i * K))
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
 
