@@ -335,8 +335,26 @@ template <typename T>
 static __global__ void xconst_kernel(const T* x, int64_t n, double beta, double* partials) {
   __shared__ double red[256];
   double s = 0.0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-    s += xpow_term(x[i], beta);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if constexpr (sizeof(T) == 4) {
+    // four entries per load and four independent fp64 partials (the single
+    // DADD chain made this pass latency-bound); fixed order -> deterministic
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+      const int64_t n4 = n / 4;
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      for (int64_t i = i0; i < n4; i += stride) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+        s += xpow_term(v.x, beta);
+        s1 += xpow_term(v.y, beta);
+        s2 += xpow_term(v.z, beta);
+        s3 += xpow_term(v.w, beta);
+      }
+      s = (s + s1) + (s2 + s3);
+      i0 += n4 * 4;
+    }
+  }
+  for (int64_t i = i0; i < n; i += stride) s += xpow_term(x[i], beta);
   red[threadIdx.x] = s;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
