@@ -1,8 +1,7 @@
 // Drop-in for reference include/ntf/unfold.hpp (unfold.cpp): the MU-unfold
 // comparison path.  unfold / refold / khatri_rao are host utilities; the CP
-// sweep and fit run on the GPU (explicit Khatri-Rao + unfolding + cuBLAS,
-// ntfg_cp_mu_unfold_*).  The Tucker MU-unfold baseline is not part of this
-// build: those two entry points throw DomainError.
+// and Tucker sweeps and fits run on the GPU (explicit Khatri-Rao / unfolding +
+// cuBLAS GEMMs + refold, ntfg_cp_mu_unfold_* and ntfg_tucker_mu_unfold_*).
 #pragma once
 
 #include <cstddef>

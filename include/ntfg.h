@@ -153,6 +153,17 @@ ntfg_status ntfg_cp_mu_unfold_fit(ntfg_context* ctx, const ntfg_fit_config* cfg,
 ntfg_status ntfg_cp_mu_unfold_sweep(ntfg_context* ctx, int32_t precision, double beta, double eps,
                                     uint32_t order, const uint64_t* dims, const double* x, uint64_t rank,
                                     double* factors_inout);
+/* mu_unfold_tucker_fit / mu_unfold_tucker_sweep (reference unfold.hpp:39-42,
+ * unfold.cpp:137-185,199-209): core then factors ascending, every mode product
+ * through an explicit unfolding + cuBLAS GEMM + refold. Core ranks from
+ * cfg->ranks (fit) / ranks (sweep). */
+ntfg_status ntfg_tucker_mu_unfold_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, uint32_t order,
+                                      const uint64_t* dims, const void* x, int32_t x_dtype, int32_t x_location,
+                                      double* core_inout, double* factors_inout, ntfg_trace_row* trace,
+                                      uint64_t* trace_len);
+ntfg_status ntfg_tucker_mu_unfold_sweep(ntfg_context* ctx, int32_t precision, double beta, double eps,
+                                        uint32_t order, const uint64_t* dims, const uint64_t* ranks,
+                                        const double* x, double* core_inout, double* factors_inout);
 
 /* ---- data ingestion and generation (reference io.hpp / io.cpp) ---------------
  * ctx may be NULL for host-only calls (location NTFG_HOST). */

@@ -11,7 +11,7 @@ from .api import (  # noqa: F401
     block_factor_update, cp_block_update_anchored, cp_contract, cp_objective, cp_reconstruct,
     default_context, jcomm_fit, jcomm_fit_coo, jcomm_inner_core_update, jcomm_inner_factor_update,
     jcomm_inner_update, jcomm_outer_step, jcomm_tucker_outer_step, make_jcomm_reference,
-    make_jcomm_tucker_reference, mu_unfold_cp_fit, mu_unfold_cp_sweep, tucker_bcomm_fit, tucker_bcomm_sweep, tucker_factor_contract,
+    make_jcomm_tucker_reference, mu_unfold_cp_fit, mu_unfold_cp_sweep, mu_unfold_tucker_fit, mu_unfold_tucker_sweep, tucker_bcomm_fit, tucker_bcomm_sweep, tucker_factor_contract,
     tucker_jcomm_fit, tucker_multimode_contract, tucker_objective, tucker_reconstruct,
     validate_fit_config)
 

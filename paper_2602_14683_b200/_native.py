@@ -85,6 +85,9 @@ _SIGS = {
     "ntfg_cp_mu_unfold_fit": [_V, C.POINTER(FitConfigC), C.c_uint32, _U, _V, C.c_int32, C.c_int32, _P,
                               C.POINTER(TraceRowC), _U],
     "ntfg_cp_mu_unfold_sweep": [_V, C.c_int32, C.c_double, C.c_double, C.c_uint32, _U, _P, C.c_uint64, _P],
+    "ntfg_tucker_mu_unfold_fit": [_V, C.POINTER(FitConfigC), C.c_uint32, _U, _V, C.c_int32, C.c_int32, _P, _P,
+                                  C.POINTER(TraceRowC), _U],
+    "ntfg_tucker_mu_unfold_sweep": [_V, C.c_int32, C.c_double, C.c_double, C.c_uint32, _U, _U, _P, _P, _P],
     "ntfg_ctf1_header": [C.c_char_p, C.POINTER(C.c_uint32), _U, C.c_uint32, C.c_uint64],
     "ntfg_ctf1_read": [_V, C.c_char_p, _V, C.c_int32, C.c_int32, C.c_uint64],
     "ntfg_ctf1_write": [_V, C.c_char_p, C.c_uint32, _U, _V, C.c_int32, C.c_int32],

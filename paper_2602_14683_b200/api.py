@@ -436,6 +436,36 @@ def mu_unfold_cp_sweep(f, x, beta: float, eps: float, precision: str = "f64", ct
     return _split(flat, [a.shape for a in f])
 
 
+def mu_unfold_tucker_fit(x, init, cfg: FitConfig, ctx: Optional[Context] = None) -> TuckerFitResult:
+    """Classical matricized Tucker MU baseline (reference unfold.cpp:137-185,
+    199-209): every mode product through an explicit unfolding + cuBLAS GEMM."""
+    ctx = ctx or default_context()
+    dims, xp, xdt, xloc, keep = _x_arg(x)
+    core, fs = _check_tucker(init[0], init[1], dims, "mu_unfold_tucker_fit")
+    cfgc, keep_r = cfg._c()
+    _check(N.load().ntfg_validate_fit_config(C.byref(cfgc)))
+    c = core.copy()
+    f = _cat(fs)
+    rows = (N.TraceRowC * (int(cfg.max_iters) + 1))()
+    n = C.c_uint64(0)
+    _check(N.load().ntfg_tucker_mu_unfold_fit(ctx.h, C.byref(cfgc), len(dims), _u64(dims).ctypes.data_as(_UP), xp,
+                                              xdt, xloc, _dp(c), _dp(f), rows, C.byref(n)))
+    return TuckerFitResult((c, _split(f, [a.shape for a in fs])), _trace(rows, n.value))
+
+
+def mu_unfold_tucker_sweep(core, factors, x, beta: float, eps: float, precision: str = "f64", ctx=None):
+    """mu_unfold_tucker_sweep (reference unfold.cpp:137-185) on the GPU."""
+    ctx = ctx or default_context()
+    x = _f64(x)
+    core, fs = _check_tucker(core, factors, list(x.shape), "mu_unfold_tucker_sweep")
+    c = core.copy()
+    f = _cat(fs)
+    _check(N.load().ntfg_tucker_mu_unfold_sweep(ctx.h, _prec(precision), float(beta), float(eps), x.ndim,
+                                                _u64(list(x.shape)).ctypes.data_as(_UP),
+                                                _u64(list(core.shape)).ctypes.data_as(_UP), _dp(x), _dp(c), _dp(f)))
+    return c, _split(f, [a.shape for a in fs])
+
+
 # ---------------------------------------------------------------------------
 # CP step level (reference cp.hpp:30-74)
 

@@ -17,6 +17,10 @@ void cp_reconstruct(Context&, int, uint32_t, const uint64_t*, uint64_t, const do
 void cp_mu_unfold_fit(Context&, const ntfg_fit_config&, uint32_t, const uint64_t*, const void*, int, int, double*,
                       ntfg_trace_row*, uint64_t*);
 void cp_mu_unfold_sweep(Context&, int, double, double, uint32_t, const uint64_t*, const double*, uint64_t, double*);
+void tucker_mu_unfold_fit(Context&, const ntfg_fit_config&, uint32_t, const uint64_t*, const void*, int, int, double*,
+                          double*, ntfg_trace_row*, uint64_t*);
+void tucker_mu_unfold_sweep(Context&, int, double, double, uint32_t, const uint64_t*, const uint64_t*, const double*,
+                            double*, double*);
 // io_api.cu
 void ctf1_header_api(const char*, uint32_t*, uint64_t*, uint32_t, uint64_t);
 void ctf1_read(Context*, const char*, void*, int, int, uint64_t);
@@ -227,6 +231,26 @@ NTFG_API ntfg_status ntfg_cp_mu_unfold_sweep(ntfg_context* ctx, int32_t precisio
   return with_ctx(ctx, [&](ntfg::Context& c) {
     need(dims, "dims"); need(x, "x"); need(factors, "factors");
     ntfg::cp_mu_unfold_sweep(c, precision, beta, eps, order, dims, x, rank, factors);
+  });
+}
+
+NTFG_API ntfg_status ntfg_tucker_mu_unfold_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, uint32_t order,
+                                               const uint64_t* dims, const void* x, int32_t x_dtype,
+                                               int32_t x_location, double* core, double* factors,
+                                               ntfg_trace_row* trace, uint64_t* trace_len) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(cfg, "cfg"); need(dims, "dims"); need(x, "x"); need(core, "core"); need(factors, "factors");
+    need(trace, "trace"); need(trace_len, "trace_len");
+    ntfg::tucker_mu_unfold_fit(c, *cfg, order, dims, x, x_dtype, x_location, core, factors, trace, trace_len);
+  });
+}
+
+NTFG_API ntfg_status ntfg_tucker_mu_unfold_sweep(ntfg_context* ctx, int32_t precision, double beta, double eps,
+                                                 uint32_t order, const uint64_t* dims, const uint64_t* ranks,
+                                                 const double* x, double* core, double* factors) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(ranks, "ranks"); need(x, "x"); need(core, "core"); need(factors, "factors");
+    ntfg::tucker_mu_unfold_sweep(c, precision, beta, eps, order, dims, ranks, x, core, factors);
   });
 }
 

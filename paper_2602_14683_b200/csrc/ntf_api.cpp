@@ -766,12 +766,35 @@ CpFitResult mu_unfold_cp_fit(const DenseTensor& x, CpFactors init, const FitConf
     return out;
 }
 
-TuckerModel mu_unfold_tucker_sweep(const TuckerModel&, const DenseTensor&, const BetaParam&, double) {
-    throw DomainError("mu_unfold_tucker_sweep: the Tucker MU-unfold baseline is not part of the B200 build");
+TuckerModel mu_unfold_tucker_sweep(const TuckerModel& m, const DenseTensor& x, const BetaParam& p, double eps) {
+    require_dims(m.factors, x, "mu_unfold_tucker_sweep");
+    TuckerModel out = m;
+    auto flat = concat(out.factors);
+    const auto dims = u64(x.shape());
+    const auto ranks = u64(m.core.shape());
+    if (ranks.size() != dims.size()) throw ShapeError("TuckerModel: core order does not match factor count");
+    ok(ntfg_tucker_mu_unfold_sweep(ctx(), NTFG_F64, p.beta(), eps, std::uint32_t(dims.size()), dims.data(),
+                                   ranks.data(), x.data(), out.core.data(), flat.data()));
+    split_into(flat, out.factors);
+    return out;
 }
 
-TuckerFitResult mu_unfold_tucker_fit(const DenseTensor&, TuckerModel, const FitConfig&) {
-    throw DomainError("mu_unfold_tucker_fit: the Tucker MU-unfold baseline is not part of the B200 build");
+TuckerFitResult mu_unfold_tucker_fit(const DenseTensor& x, TuckerModel init, const FitConfig& cfg) {
+    validate_fit_config(cfg);
+    require_dims(init.factors, x, "mu_unfold_tucker_fit");
+    FitConfig c2 = cfg;
+    c2.ranks = init.core.shape();
+    std::vector<std::uint64_t> keep;
+    ntfg_fit_config c = to_c(c2, keep);
+    auto flat = concat(init.factors);
+    std::vector<ntfg_trace_row> rows(cfg.max_iters + 1);
+    std::uint64_t n = 0;
+    const auto dims = u64(x.shape());
+    ok(ntfg_tucker_mu_unfold_fit(ctx(cfg.device), &c, std::uint32_t(dims.size()), dims.data(), x.data(), 0,
+                                 NTFG_HOST, init.core.data(), flat.data(), rows.data(), &n));
+    TuckerFitResult out{std::move(init), trace_of(rows, n)};
+    split_into(flat, out.model.factors);
+    return out;
 }
 
 }  // namespace ntf

@@ -63,3 +63,39 @@ def test_unfold_fit_fp32():
     b = ntf.mu_unfold_cp_fit(x, init, ntf.FitConfig(beta=0.5, rank=8, max_iters=10, precision="f64"))
     assert relm(a.model, b.model) < 1e-4
     assert O.rel_err([t.loss for t in a.trace], [t.loss for t in b.trace]) < 1e-5
+
+
+# ---- Tucker MU-unfold (reference unfold.cpp:137-185) ---------------------------------
+
+def tucker_problem(dims, ranks, seed):
+    rng = np.random.default_rng(seed)
+    core = rng.random(ranks)
+    fs = [rng.random((d, j)) for d, j in zip(dims, ranks)]
+    x = O.tucker_reconstruct(core, fs) * rng.gamma(10.0, 0.1, size=dims)
+    init = (0.1 + rng.random(ranks), [0.1 + rng.random((d, j)) for d, j in zip(dims, ranks)])
+    return x, init
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 1.5])
+@pytest.mark.parametrize("dims,ranks", [((9, 7, 6), (3, 2, 4)), ((5, 4, 6, 3), (2, 3, 2, 2))])
+def test_mu_unfold_tucker_sweep_equals_block_sweep(beta, dims, ranks):
+    # the matricized sweep is the same MM map as the contraction-based block
+    # sweep (core first, then factors ascending), up to summation order
+    x, (core, fs) = tucker_problem(dims, ranks, 3)
+    c1, f1 = ntf.mu_unfold_tucker_sweep(core, fs, x, beta, EPS)
+    oc, of = O.tucker_bcomm_sweep((core, fs), x, beta, EPS)
+    assert O.rel_err(c1, oc) < 1e-11
+    assert max(O.rel_err(a, b) for a, b in zip(f1, of)) < 1e-11
+
+
+@pytest.mark.parametrize("beta", [0.5, 1.0])
+def test_mu_unfold_tucker_fit_matches_bcomm(beta):
+    x, init = tucker_problem((10, 8, 6), (3, 3, 2), 5)
+    cfg = ntf.FitConfig(beta=beta, rank=1, ranks=[3, 3, 2], max_iters=12)
+    a = ntf.mu_unfold_tucker_fit(x, init, cfg)
+    b = ntf.tucker_bcomm_fit(x, init, cfg)
+    assert O.rel_err([t.loss for t in a.trace], [t.loss for t in b.trace]) < 1e-10
+    assert O.rel_err(a.model[0], b.model[0]) < 1e-10
+    f32 = ntf.mu_unfold_tucker_fit(x, init, ntf.FitConfig(beta=beta, rank=1, ranks=[3, 3, 2], max_iters=12,
+                                                          precision="f32"))
+    assert O.rel_err([t.loss for t in f32.trace], [t.loss for t in b.trace]) < 1e-5
