@@ -102,7 +102,7 @@ __device__ __forceinline__ void rt_split_pair(float a, float b, uint32_t& hi, ui
 // (a tile's 32 rows then share the slower coordinates: H = G(r) * A_f rows,
 // G = product of the slower modes' rows, computed once per tile); 0 = generic.
 template <int RP, int BK, int NPRE>
-static __global__ void __launch_bounds__(kRtThreads, 2) recon_tile_kernel(const ReconParams<float> p) {
+static __global__ void __launch_bounds__(kRtThreads, 3) recon_tile_kernel(const ReconParams<float> p) {
   using L = RtSmem<RP>;
   constexpr int HS = L::HS;
   constexpr int HI = RP * kRtRows / kRtThreads;  // H items per thread per tile (same r for all)
