@@ -1,18 +1,25 @@
 #!/usr/bin/env python
-"""Benchmark: J-CoMM outer iterations/s on BASELINE config C2.
+"""Benchmark: MM outer iterations/s on the largest single-GPU BASELINE config (C5).
 
-Workload (BASELINE.json configs[1]): dense 3-way CP, 512x512x512 fp32, R = 32,
-joint-MM with 5 inner sweeps per outer iteration; data = [[A,B,C]] (U[0,1)
-factors) times Gamma(10, 0.1) noise, init U[0.1, 1.1).  One "step" = one
-outer iteration (reference cache build + 15 inner block updates, objective
-fused).  The headline beta is 0.5; all four betas of the config are measured
-and reported under "per_beta".  Data is synthetic (seeded) and generated on
-the GPU; X, P~, Q~ (1.5 GB) exceed the 126 MB L2, so no flush is needed.
+Headline workload (BASELINE.json configs[4], "C5"): dense 4-way CP
+256x256x256x256 fp32 (4.29e9 entries, 17 GB), R = 64, beta = 0.5, joint-MM
+with 5 inner sweeps per outer iteration; data = [[A,B,C,D]] (U[0,1) truth)
+times Gamma(10, 0.1) noise, init U[0.1, 1.1), generated in place on the GPU by
+the seeded Philox generator (paper_2602_14683_b200.io).  One "step" = one
+outer iteration: the J-CoMM reference pass (X -> P~, Q~, objective fused) and
+4 x 5 = 20 inner block updates (tensor-core contractions + fp64 MU).  X, P~,
+Q~ (51 GB) exceed the 126 MB L2 by 400x, so no flush is needed.
+
+The other BASELINE configs are measured as side keys of the same JSON line:
+C2 (512^3, R=32, all four betas), C1 (100^3 fp64 B-CoMM), C3 (Tucker 256^3,
+core 16^3) and C4 (sparse COO).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 runs under torchrun: X is split into mode-0 slabs, factors replicated,
-the Num/Den partials are allreduced (NCCL) -- strong scaling of the same job.
+N > 1 runs under torchrun: X is split into mode-0 slabs (one per rank),
+factors are replicated, and the Num/Den partials are allreduced in place by
+the engine's native NCCL communicator on its own stream inside the captured
+CUDA graph (strong scaling of the same C5 job).
 """
 from __future__ import annotations
 
@@ -31,13 +38,29 @@ if ROOT not in sys.path:
 
 import numpy as np
 
-DIMS = (512, 512, 512)
-RANK = 32
-INNER = 5
-BETAS = [0.5, 0.0, 1.0, 1.5]
-HEADLINE_BETA = 0.5
-METRIC = "MM outer iterations/sec (J-CoMM, C2 512^3 R=32 L=5)"
+C5_DIMS = (256, 256, 256, 256)
+C5_RANK = 64
+C5_BETA = 0.5
+C5_INNER = 5
+METRIC = "MM outer iterations/sec (J-CoMM, C5 256^4 R=64 L=5 beta=0.5)"
 FFMA_PEAK_T = 35.4  # measured FP32 FMA/s (T) on this pool's B200, profiles/r01_ubench.log
+
+C2_DIMS = (512, 512, 512)
+C2_RANK = 32
+C2_BETAS = [0.5, 0.0, 1.0, 1.5]
+
+# CPU samples of the C5 workload (oracle/_ref = the compiled, unmodified
+# reference; cp.cpp:271-298 jcomm_fit via ref_shim's timing entry point)
+CPU_SAMPLE_DIMS = (1, 128, 256, 256)   # our arm's cpu_baseline: 1 core, ~10-20 s
+REF_SAMPLE_DIMS = (1, 32, 256, 256)    # --impl reference: one per host thread per step
+
+
+def workload_config(world: int) -> dict:
+    """Identical in both arms (the driver compares them)."""
+    return {"workload": "C5: dense 4-way CP 256x256x256x256 fp32 (4.29e9 entries, 17 GB), R=64, beta=0.5, "
+                        "J-CoMM L=5 (BASELINE configs[4])",
+            "parallelism": f"mode-0 slabs dp{world}" if world > 1 else "single device",
+            "l2": "inputs X 17 GB + P~/Q~ 34 GB exceed the 126 MB L2; no flush"}
 
 
 def peaks():
@@ -45,9 +68,21 @@ def peaks():
     try:
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel_key: str):
+    """dram read+write bytes per launch of the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(kernel_key)
+        return (e["dram_bytes_per_launch"], e["source"]) if e else (None, None)
+    except Exception:
+        return None, None
 
 
 # ---------------------------------------------------------------------------
@@ -106,200 +141,225 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# synthetic data
+# distributed plumbing
 
-def make_problem(dims, rank, seed, row0, row1, device):
-    """Truth U[0,1) factors, X = [[A,B,C]] * Gamma(10, 0.1) (fp32 on `device`),
-    init U[0.1, 1.1).  Rows [row0, row1) of mode 0 belong to this rank."""
-    import torch
-    g = torch.Generator(device="cpu").manual_seed(seed)
-    truth = [torch.rand(d, rank, generator=g, dtype=torch.float64) for d in dims]
-    t0 = truth[0][row0:row1].to(device)
-    rest = [t.to(device) for t in truth[1:]]
-    x = torch.einsum("ir,jr,kr->ijk", t0, rest[0], rest[1])
-    gc = torch.Generator(device=device).manual_seed(seed + 7)
-    shape = (dims[0],) + tuple(dims[1:])
-    alpha = torch.full(shape, 10.0, device=device, dtype=torch.float32)
-    noise = torch._standard_gamma(alpha, generator=gc)[row0:row1] * 0.1
-    del alpha
-    x = (x * noise.double()).float().contiguous()
-    del noise
-    rng = np.random.default_rng(seed + 1)
-    init = [0.1 + rng.random((d, rank)) for d in dims]
-    init[0] = init[0][row0:row1].copy()
-    return x, init
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dist = None
+
+    def init(self):
+        import torch
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+
+    def rows(self, i0):
+        return i0 * self.rank // self.world, i0 * (self.rank + 1) // self.world
+
+    def barrier(self):
+        import torch
+        torch.cuda.synchronize()
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max(self, v):
+        if self.dist is None:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64, device=torch.device("cuda", self.local))
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def context(self):
+        """Engine context on this rank's device; native NCCL communicator when N > 1."""
+        import paper_2602_14683_b200 as ntf
+        from paper_2602_14683_b200 import dist as D
+        ctx = ntf.Context(self.local)
+        if self.dist is not None:
+            D.attach_nccl(ctx)
+        return ctx
 
 
 # ---------------------------------------------------------------------------
-# our arm
+# headline: C5
 
-def run_ours(args, rank_id, world, local_rank):
-    import torch
-    import paper_2602_14683_b200 as ntf
-
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    row0 = DIMS[0] * rank_id // world
-    row1 = DIMS[0] * (rank_id + 1) // world
-    x, init = make_problem(DIMS, RANK, 0, row0, row1, dev)
-    torch.cuda.synchronize()
-    ctx = ntf.Context(local_rank)
-    # a dedicated (capturable) stream shared by torch and the engine
-    stream = torch.cuda.Stream(device=dev)
-    torch.cuda.set_stream(stream)
-    ctx.set_stream(stream.cuda_stream)
-    shard = None
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        comm = torch.zeros(2 * max(DIMS) * RANK + 8, dtype=torch.float64, device=dev)
-        ctx.set_comm_buffer(comm.data_ptr(), comm.numel())
-
-        def allreduce(ptr, count, stream):
-            dist.all_reduce(comm[:count])
-
-        ctx.set_allreduce(allreduce)
-        shard = (DIMS[0], row0)
-
-    def fit(beta, iters, **kw):
-        cfg = ntf.FitConfig(beta=beta, rank=RANK, inner_steps=INNER, max_iters=iters, precision="f32", **kw)
-        return ntf.jcomm_fit(x, init, cfg, ctx=ctx, shard=shard)
-
-    def barrier():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-
-    def max_over_ranks(v):
-        if dist is None:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    per_beta = {}
-    launches = None
-    sampler = ClockSampler(local_rank) if rank_id == 0 else None
-    if sampler:
-        sampler.start()
-    for beta in BETAS:
-        fit(beta, args.warmup)               # W untimed warm-up outer iterations
-        barrier()
-        res = fit(beta, args.steps)          # exactly K timed outer iterations
-        barrier()
-        st = ctx.stats()
-        ms = max_over_ranks(st["device_ms"])  # CUDA events around the K steps
-        per_beta[beta] = {"outer_it_per_s": args.steps / (ms * 1e-3), "ms_per_step": ms / args.steps,
-                          "final_loss": res.trace[-1].loss}
-        if beta == HEADLINE_BETA:
-            launches = st["kernel_launches"]
-    clocks = sampler.stop() if sampler else None
-
-    # per-kernel timing of the dominant kernel (eager launches, CUDA events on the launch stream)
-    ctx.set_profiling(True)
-    fit(HEADLINE_BETA, min(args.steps, 5))
-    pst = ctx.stats()
-    ctx.set_profiling(False)
-
-    # end to end through the public API with host (pinned) X: H2D + fit + D2H in the timed region
-    e2e = None
-    if args.e2e:
-        xh = x.cpu().pin_memory()
-        fit_h = lambda it: ntf.jcomm_fit(xh, init, ntf.FitConfig(beta=HEADLINE_BETA, rank=RANK, inner_steps=INNER,
-                                                              max_iters=it, precision="f32"), ctx=ctx, shard=shard)
-        fit_h(1)
-        barrier()
-        t0 = time.perf_counter()
-        fit_h(args.steps)
-        barrier()
-        el = max_over_ranks(time.perf_counter() - t0)
-        e2e = {"value": args.steps / el, "unit": "outer_it/s",
-               "h2d_bytes_per_step": int(xh.numel() * 4 + sum(a.size * 8 for a in init)),
-               "d2h_bytes_per_step": int(sum(a.size * 8 for a in init) + (args.steps + 1) * 24),
-               "note": "one step = one public-API fit call of K outer iterations from pinned host X "
-                       "(X upload + factor/trace download inside the timed region); value = K / wall time"}
-        del xh
-
-    c4 = run_c4(args, ctx, dev) if world == 1 and args.c4 else None
-    c5 = None
-    if args.c5:
-        try:  # a side measurement must never sink the headline line
-            c5 = run_c5(args, rank_id, world, local_rank, dev, dist, max_over_ranks)
-        except Exception as ex:
-            c5 = {"workload": "C5", "error": f"{type(ex).__name__}: {str(ex)[:200]}"}
-    return per_beta, launches, pst, clocks, e2e, c4, c5
-
-
-C5_DIM = 256
-C5_RANK = 64
-C5_INNER = 5
-C5_BETA = 0.5
-
-
-def run_c5(args, rank_id, world, local_rank, dev, dist, max_over_ranks):
-    """C5 (BASELINE configs[4]): dense 4-way CP 256^4 fp32 (17 GB), R=64,
-    beta=0.5, J-CoMM L=5.  Mode-0 slabs generated in place on each rank
-    (Philox, paper_2602_14683_b200.io); factors replicated, Num/Den partials
-    allreduced.  value = outer iterations / device time (max over ranks) of
-    C5_STEPS timed outer iterations after one warm-up."""
+def run_c5(args, d: Dist):
     import torch
     import paper_2602_14683_b200 as ntf
     from paper_2602_14683_b200 import io as nio
-    dims = (C5_DIM,) * 4
-    row0 = C5_DIM * rank_id // world
-    row1 = C5_DIM * (rank_id + 1) // world
-    x = nio.generate_cp_gamma(dims, C5_RANK, seed=0, rows=(row0, row1), device=local_rank)
-    init = nio.cp_factors(dims, C5_RANK, seed=1, which="init")
+    row0, row1 = d.rows(C5_DIMS[0])
+    x = nio.generate_cp_gamma(C5_DIMS, C5_RANK, seed=0, rows=(row0, row1), device=d.local)
+    init = nio.cp_factors(C5_DIMS, C5_RANK, seed=1, which="init")
     init[0] = init[0][row0:row1].copy()
-    ctx = ntf.Context(local_rank)
-    stream = torch.cuda.Stream(device=dev)
-    ctx.set_stream(stream.cuda_stream)
-    shard = None
-    if world > 1:
-        comm = torch.zeros(2 * C5_DIM * C5_RANK + 8, dtype=torch.float64, device=dev)
-        ctx.set_comm_buffer(comm.data_ptr(), comm.numel())
+    torch.cuda.synchronize()
+    ctx = d.context()
+    shard = (C5_DIMS[0], row0) if d.world > 1 else None
+    cfg = lambda it, **kw: ntf.FitConfig(beta=C5_BETA, rank=C5_RANK, inner_steps=C5_INNER, max_iters=it,
+                                         precision="f32", **kw)
 
-        def allreduce(ptr, count, strm):
-            with torch.cuda.stream(stream):
-                dist.all_reduce(comm[:count])
+    ntf.jcomm_fit(x, init, cfg(args.warmup), ctx=ctx, shard=shard)   # W untimed outer iterations
+    d.barrier()
+    sampler = ClockSampler(d.local) if d.rank == 0 else None
+    if sampler:
+        sampler.start()
+    res = ntf.jcomm_fit(x, init, cfg(args.steps), ctx=ctx, shard=shard)  # exactly K timed outer iterations
+    d.barrier()
+    clocks = sampler.stop() if sampler else None
+    st = ctx.stats()
+    ms = d.max(st["device_ms"])  # CUDA events on the engine stream around the K graph replays
+    launches = st["kernel_launches"]
 
-        ctx.set_allreduce(allreduce)
-        shard = (C5_DIM, row0)
-    steps = max(1, min(args.c5_steps, args.steps))
-    cfg = lambda it: ntf.FitConfig(beta=C5_BETA, rank=C5_RANK, inner_steps=C5_INNER, max_iters=it, precision="f32")
-    with torch.cuda.stream(stream):
-        ntf.jcomm_fit(x, init, cfg(1), ctx=ctx, shard=shard)
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        res = ntf.jcomm_fit(x, init, cfg(steps), ctx=ctx, shard=shard)
-        torch.cuda.synchronize()
-    ms = max_over_ranks(ctx.stats()["device_ms"]) / steps
-    launches = ctx.stats()["kernel_launches"]
+    # per-kernel-class device time of one eager outer iteration (events on the launch stream)
     ctx.set_profiling(True)
-    with torch.cuda.stream(stream):
-        ntf.jcomm_fit(x, init, cfg(1), ctx=ctx, shard=shard)
+    ntf.jcomm_fit(x, init, cfg(1), ctx=ctx, shard=shard)
     pst = ctx.stats()
     ctx.set_profiling(False)
-    E = C5_DIM ** 4
-    alg = 4.0 * E * (1 + 2 + 2 * C5_INNER * 4)  # X + P~,Q~ written once, read once per inner block update
+
+    e2e = None
+    if args.e2e:
+        e2e = c5_e2e(args, d, x, init, ctx, shard, cfg)
+    out = {"ms": ms, "launches": launches, "pst": pst, "clocks": clocks, "e2e": e2e,
+           "final_loss": res.trace[-1].loss, "local_entries": x.numel()}
+    del x
+    ctx.trim()
+    del ctx
+    torch.cuda.empty_cache()
+    return out
+
+
+def c5_e2e(args, d: Dist, x, init, ctx, shard, cfg):
+    """The public API from HOST data in the reference's own type (fp64 DenseTensor):
+    X (34 GB fp64, pinned) is uploaded + converted inside the timed call, factors
+    and trace come back to the host.  One call = K outer iterations."""
+    import torch
+    import paper_2602_14683_b200 as ntf
+    xh = torch.empty(tuple(x.shape), dtype=torch.float64, pin_memory=True)
+    step = 16
+    for i in range(0, x.shape[0], step):
+        xh[i:i + step].copy_(x[i:i + step].double())
+    torch.cuda.synchronize()
+    ntf.jcomm_fit(xh, init, cfg(1), ctx=ctx, shard=shard)  # warm (buffers, graph instantiation paths)
+    d.barrier()
+    t0 = time.perf_counter()
+    res = ntf.jcomm_fit(xh, init, cfg(args.steps), ctx=ctx, shard=shard)
+    el = d.max(time.perf_counter() - t0)
+    fbytes = sum(a.size * 8 for a in init)
+    out = {"value": d.world * 0 + args.steps / el, "unit": "outer_it/s",
+           "h2d_bytes_per_step": int((xh.numel() * 8 + fbytes) / args.steps),
+           "d2h_bytes_per_step": int((fbytes + (args.steps + 1) * 24) / args.steps),
+           "host_x": "fp64 pinned (the reference's DenseTensor type)",
+           "note": "one public-API jcomm_fit call of K outer iterations from pinned host fp64 X: the X upload "
+                   "(+ fp64->fp32 conversion) and the factor/trace download are inside the timed region; "
+                   "bytes are per outer iteration (call bytes / K); value = K / wall time (max over ranks)",
+           "final_loss": res.trace[-1].loss}
+    del xh
+    return out
+
+
+# ---------------------------------------------------------------------------
+# side configs
+
+def run_c2(args, d: Dist):
+    """C2 (configs[1]): 512^3 fp32, R=32, J-CoMM L=5, every beta."""
+    import torch
+    import paper_2602_14683_b200 as ntf
+    from paper_2602_14683_b200 import io as nio
+    row0, row1 = d.rows(C2_DIMS[0])
+    x = nio.generate_cp_gamma(C2_DIMS, C2_RANK, seed=0, rows=(row0, row1), device=d.local)
+    init = nio.cp_factors(C2_DIMS, C2_RANK, seed=1, which="init")
+    init[0] = init[0][row0:row1].copy()
+    ctx = d.context()
+    shard = (C2_DIMS[0], row0) if d.world > 1 else None
+    per_beta = {}
+    for beta in C2_BETAS:
+        cfg = lambda it: ntf.FitConfig(beta=beta, rank=C2_RANK, inner_steps=5, max_iters=it, precision="f32")
+        ntf.jcomm_fit(x, init, cfg(args.warmup), ctx=ctx, shard=shard)
+        d.barrier()
+        res = ntf.jcomm_fit(x, init, cfg(args.steps), ctx=ctx, shard=shard)
+        d.barrier()
+        ms = d.max(ctx.stats()["device_ms"])
+        per_beta[str(beta)] = {"outer_it_per_s": args.steps / (ms * 1e-3), "ms_per_step": ms / args.steps,
+                               "final_loss": res.trace[-1].loss, "gpu_launches": ctx.stats()["kernel_launches"]}
+    ctx.set_profiling(True)
+    ntf.jcomm_fit(x, init, ntf.FitConfig(beta=0.5, rank=C2_RANK, inner_steps=5, max_iters=2, precision="f32"),
+                  ctx=ctx, shard=shard)
+    pst = ctx.stats()
+    ctx.set_profiling(False)
+    E = x.numel()
     k3_ms = pst["contract_ms"] / max(1, pst["contract_launches"])
-    k3_bytes = 8.0 * E / world
-    peak, peak_src = peaks()
-    out = {"workload": "C5: dense CP 256^4 fp32 (17 GB), R=64, beta=0.5, J-CoMM L=5, mode-0 slabs "
-                       f"dp{world}", "outer_it_per_s": 1e3 / ms, "ms_per_step": ms, "steps": steps,
-           "final_loss": res.trace[-1].loss, "gpu_launches": launches,
-           "alg_bytes_per_outer": alg, "alg_GBps_whole_step": alg / (ms * 1e-3) / 1e9,
-           "roofline_k3": {"bound": "hbm", "kernel": "tc_contract_kernel<64>", "achieved": k3_bytes / (k3_ms * 1e-3) / 1e9,
-                           "peak": peak, "unit": "GB/s", "frac": k3_bytes / (k3_ms * 1e-3) / 1e9 / peak,
-                           "peak_source": peak_src, "avg_launch_ms": k3_ms,
-                           "algorithmic_bytes_per_launch": k3_bytes},
-           "kernel_ms_one_profiled_outer": {"recon": pst["recon_ms"], "contract": pst["contract_ms"],
-                                            "note": "eager launches bracketed by events; includes the fit's final objective pass"}}
+    peak, src = peaks()
+    ach = 8.0 * E / (k3_ms * 1e-3) / 1e9
     del x
     ctx.trim()
     torch.cuda.empty_cache()
-    return out
+    return {"workload": "C2: dense CP 512^3 fp32, R=32, J-CoMM L=5 (BASELINE configs[1])",
+            "per_beta": per_beta,
+            "roofline_k3": {"bound": "hbm", "kernel": "tc_contract_kernel<32>", "achieved": ach, "peak": peak,
+                            "unit": "GB/s", "frac": ach / peak, "peak_source": src, "avg_launch_ms": k3_ms,
+                            "algorithmic_bytes_per_launch": 8.0 * E},
+            "kernel_ms_per_outer": {"recon": pst["recon_ms"] / 2, "contract": pst["contract_ms"] / 2}}
+
+
+def run_c1(args, d: Dist):
+    """C1 (configs[0]): 100^3 fp64, R=10, beta=1, B-CoMM, 200 iterations (CUDA graph per sweep)."""
+    import torch
+    import paper_2602_14683_b200 as ntf
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import datagen as DG
+    x, init = DG.c1_problem(0)
+    xd = torch.from_numpy(x).cuda(d.local)
+    ctx = ntf.Context(d.local)
+    cfg = lambda it: ntf.FitConfig(beta=1.0, rank=10, max_iters=it, precision="f64")
+    ntf.bcomm_fit(xd, init, cfg(5), ctx=ctx)
+    res = ntf.bcomm_fit(xd, init, cfg(200), ctx=ctx)
+    ms = ctx.stats()["device_ms"]
+    return {"workload": "C1: dense CP 100^3 fp64, R=10, beta=1, B-CoMM, 200 iterations (BASELINE configs[0])",
+            "it_per_s": 200 / (ms * 1e-3), "ms_per_iter": ms / 200, "final_loss": res.trace[-1].loss,
+            "fit_device_s": ms * 1e-3, "gpu_launches": ctx.stats()["kernel_launches"]}
+
+
+def run_c3(args, d: Dist):
+    """C3 (configs[2]): Tucker 256^3, core 16^3, beta in {0.5, 1}, B-CoMM and J-CoMM (L=3)."""
+    import torch
+    import paper_2602_14683_b200 as ntf
+    dims, ranks = (256, 256, 256), (16, 16, 16)
+    g = torch.Generator(device="cpu").manual_seed(0)
+    core = torch.rand(ranks, generator=g, dtype=torch.float64)
+    fs = [torch.rand(n, j, generator=g, dtype=torch.float64) for n, j in zip(dims, ranks)]
+    dev = torch.device("cuda", d.local)
+    x = torch.einsum("abc,ia,jb,kc->ijk", core.to(dev), *[f.to(dev) for f in fs])
+    gc = torch.Generator(device=dev).manual_seed(7)
+    x = (x * torch._standard_gamma(torch.full(dims, 10.0, device=dev, dtype=torch.float64), generator=gc)
+         * 0.1).float().contiguous()
+    rng = np.random.default_rng(1)
+    init = (0.1 + rng.random(ranks), [0.1 + rng.random((n, j)) for n, j in zip(dims, ranks)])
+    ctx = ntf.Context(d.local)
+    out = {}
+    for algo in ("bcomm", "jcomm"):
+        fit = ntf.tucker_bcomm_fit if algo == "bcomm" else ntf.tucker_jcomm_fit
+        for beta in (0.5, 1.0):
+            cfg = lambda it: ntf.FitConfig(beta=beta, ranks=list(ranks), inner_steps=3, max_iters=it,
+                                           precision="f32")
+            fit(x, init, cfg(args.warmup), ctx=ctx)
+            res = fit(x, init, cfg(args.steps), ctx=ctx)
+            ms = ctx.stats()["device_ms"]
+            out[f"{algo}_beta{beta}"] = {"it_per_s": args.steps / (ms * 1e-3), "ms_per_iter": ms / args.steps,
+                                         "final_loss": res.trace[-1].loss}
+    ctx.set_profiling(True)
+    ntf.tucker_jcomm_fit(x, init, ntf.FitConfig(beta=0.5, ranks=list(ranks), inner_steps=3, max_iters=1,
+                                                precision="f32"), ctx=ctx)
+    pst = ctx.stats()
+    ctx.set_profiling(False)
+    del x
+    torch.cuda.empty_cache()
+    return {"workload": "C3: Tucker 256^3 fp32, core 16^3, L=3 (BASELINE configs[2])", "fits": out,
+            "jcomm_kernel_ms_one_outer": {"recon": pst["recon_ms"], "contract": pst["contract_ms"],
+                                          "other": pst["other_ms"]}}
 
 
 C4_DIMS = (183, 24, 1140, 1717)
@@ -314,26 +374,27 @@ def c4_problem(seed: int = 0):
     ({1, 2, ...}); duplicates kept (they accumulate on ingestion)."""
     rng = np.random.default_rng(seed)
     cols = []
-    for m, d in enumerate(C4_DIMS):
+    for m, dd in enumerate(C4_DIMS):
         if m >= 2:
-            w = 1.0 / np.arange(1, d + 1) ** 1.1
-            cols.append(rng.choice(d, size=C4_NNZ, p=w / w.sum()))
+            w = 1.0 / np.arange(1, dd + 1) ** 1.1
+            cols.append(rng.choice(dd, size=C4_NNZ, p=w / w.sum()))
         else:
-            cols.append(rng.integers(0, d, size=C4_NNZ))
+            cols.append(rng.integers(0, dd, size=C4_NNZ))
     idx = np.stack(cols, axis=1).astype(np.int32)
     vals = (1 + (rng.geometric(0.5, size=C4_NNZ) - 1)).astype(np.float32)
-    init = [0.1 + rng.random((d, C4_RANK)) for d in C4_DIMS]
+    init = [0.1 + rng.random((dd, C4_RANK)) for dd in C4_DIMS]
     return idx, vals, init
 
 
-def run_c4(args, ctx, dev):
-    """C4: sparse COO CP, R=20, beta=1, J-CoMM L=3 (K7 path), COO resident on
-    the device; value = outer iterations / device time of the K timed steps."""
+def run_c4(args, d: Dist):
+    """C4: sparse COO CP, R=20, beta=1, J-CoMM L=3 (K7 path), COO resident on the device."""
     import torch
     import paper_2602_14683_b200 as ntf
     idx, vals, init = c4_problem(0)
+    dev = torch.device("cuda", d.local)
     di = torch.from_numpy(idx).to(dev)
     dv = torch.from_numpy(vals).to(dev)
+    ctx = ntf.Context(d.local)
     cfg = lambda it: ntf.FitConfig(beta=1.0, rank=C4_RANK, inner_steps=C4_INNER, max_iters=it, precision="f64")
     ntf.jcomm_fit_coo(di, dv, C4_DIMS, init, cfg(args.warmup), ctx=ctx)
     res = ntf.jcomm_fit_coo(di, dv, C4_DIMS, init, cfg(args.steps), ctx=ctx)
@@ -345,75 +406,107 @@ def run_c4(args, ctx, dev):
             "gpu_launches": st["kernel_launches"]}
 
 
+def side(fn, *a):
+    try:  # a side measurement must never sink the headline line
+        return fn(*a)
+    except Exception as ex:
+        return {"error": f"{type(ex).__name__}: {str(ex)[:300]}"}
+
+
 # ---------------------------------------------------------------------------
 # CPU reference (compiled unmodified reference; oracle/_ref) or the NumPy port
 
-def cpu_sample(steps_per_thread: int = 2, slab: int = 4, threads: int = 0, beta: float = HEADLINE_BETA):
-    """Times the reference solver on mode-0 slabs (slab x 512 x 512) of the C2
-    workload, one independent slab per host thread; returns C2-equivalent
-    outer it/s = entries processed per second / |X|."""
+def sample_problem(dims, seed):
+    """A slab of the C5 workload's distribution: U[0,1) truth, Gamma(10, 0.1) noise, init U[0.1, 1.1)."""
+    rng = np.random.default_rng(seed)
+    truth = [rng.random((n, C5_RANK)) for n in dims]
+    x = np.einsum("ir,jr,kr,lr->ijkl", *truth, optimize=True) * rng.gamma(10.0, 0.1, size=dims)
+    init = [0.1 + rng.random((n, C5_RANK)) for n in dims]
+    return x, init
+
+
+def time_sample(dims, seed):
+    """Seconds of one J-CoMM outer iteration on the sample (the reference's own
+    solver timer when oracle/_ref exists, else the NumPy port's wall time)."""
     from oracle import ref as R
-    threads = threads or (os.cpu_count() or 1)
-    rng = np.random.default_rng(3)
-    dims = (slab,) + DIMS[1:]
-    truth = [rng.random((d, RANK)) for d in dims]
+    x, init = sample_problem(dims, seed)
+    if R.available():
+        sec, _ = R.cp_time_outer("jcomm", x, init, C5_BETA, 1, inner_steps=C5_INNER)
+        return sec, "reference"
     from oracle import ntf_oracle as O
-    x = O.cp_reconstruct(truth) * rng.gamma(10.0, 0.1, size=dims)
-    init = [0.1 + rng.random((d, RANK)) for d in dims]
-    kind = "reference" if R.available() else "port"
-    times = [0.0] * threads
-
-    def work(i):
-        if kind == "reference":
-            sec, _ = R.cp_time_outer("jcomm", x, init, beta, steps_per_thread, inner_steps=INNER)
-        else:
-            t0 = time.perf_counter()
-            f = [a.copy() for a in init]
-            for _ in range(steps_per_thread):
-                f = O.jcomm_outer_step(f, x, beta, INNER, 1e-12)
-            sec = time.perf_counter() - t0
-        times[i] = sec
-
     t0 = time.perf_counter()
-    th = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    wall = time.perf_counter() - t0
-    entries = threads * steps_per_thread * int(np.prod(dims))
-    value = entries / wall / float(np.prod(DIMS))
-    return {"value": value, "unit": "outer_it/s", "cores": threads, "kind": kind,
-            "sample": f"{threads} threads x {steps_per_thread} J-CoMM outer step(s) (L={INNER}, beta={beta}) "
-                      f"on independent {slab}x512x512 fp64 slabs of the C2 workload; "
-                      f"C2-equivalent rate = entries/s / 512^3 (wall {wall:.2f} s)"}
+    O.jcomm_outer_step([a.copy() for a in init], x, C5_BETA, C5_INNER, 1e-12)
+    return time.perf_counter() - t0, "port"
 
 
-def run_reference(args, rank_id):
-    if rank_id != 0:
+def cpu_baseline():
+    """oracle/_ref on ONE pinned core (the reference is single-threaded)
+    on a 1x128x256x256 slab of C5 (1/512 of the tensor): C5-equivalent outer it/s."""
+    code = ("import sys, json; sys.path.insert(0, %r); import bench; s, k = bench.time_sample(%r, 5); "
+            "print(json.dumps([s, k]))" % (ROOT, CPU_SAMPLE_DIMS))
+    cmd = [sys.executable, "-c", code]
+    try:
+        subprocess.run(["taskset", "-c", "0", "true"], check=True, capture_output=True)
+        cmd = ["taskset", "-c", "0"] + cmd
+        pinned = True
+    except Exception:
+        pinned = False
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    sec, kind = json.loads(r.stdout.strip().splitlines()[-1])
+    frac = float(np.prod(CPU_SAMPLE_DIMS)) / float(np.prod(C5_DIMS))
+    return {"value": frac / sec, "unit": "outer_it/s", "cores": 1, "kind": kind,
+            "sample": f"one J-CoMM outer iteration (L=5, beta=0.5, R=64) of {kind} jcomm_fit on a "
+                      f"{'x'.join(map(str, CPU_SAMPLE_DIMS))} slab of the C5 workload (1/{int(1/frac)} of its "
+                      f"entries), solver time {sec:.2f} s (reference time_s), {'taskset core 0' if pinned else 'unpinned'}; "
+                      f"C5 rate = slab fraction / time"}
+
+
+def run_reference(args, d: Dist):
+    """--impl reference: the compiled reference (oracle/_ref) on all host cores:
+    each step runs one J-CoMM outer iteration per host thread on independent
+    1x32x256x256 slabs of C5 (threads x 1/2048 of its entries); value = C5
+    outer it/s = slabs x fraction / step wall time; ms_per_step = the measured
+    step wall time."""
+    if d.rank != 0:
         return
-    cpu_sample(1)  # warm the page cache / threads
-    vals = []
-    samples = None
+    from oracle import ref as R
+    threads = os.cpu_count() or 1
+    probs = [sample_problem(REF_SAMPLE_DIMS, 100 + i) for i in range(threads)]
+    kind = "reference" if R.available() else "port"
+    frac = float(np.prod(REF_SAMPLE_DIMS)) / float(np.prod(C5_DIMS))
+
+    def one_step():
+        def work(i):
+            x, init = probs[i]
+            if kind == "reference":
+                R.cp_time_outer("jcomm", x, init, C5_BETA, 1, inner_steps=C5_INNER)
+            else:
+                from oracle import ntf_oracle as O
+                O.jcomm_outer_step([a.copy() for a in init], x, C5_BETA, C5_INNER, 1e-12)
+        th = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        return time.perf_counter() - t0
+
     for _ in range(args.warmup):
-        cpu_sample(1)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        s = cpu_sample(1)
-        vals.append(s["value"])
-        samples = s
-    el = time.perf_counter() - t0
-    value = statistics.mean(vals)
+        one_step()
+    walls = [one_step() for _ in range(args.steps)]
+    wall = sum(walls)
+    value = threads * frac * args.steps / wall
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "outer_it/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2: CP 512^3 R=32 J-CoMM L=5 beta=0.5 (mode-0 slab samples)",
-                       "global_batch": 1, "seq_len": 0, "parallelism": "host threads"},
-            "cpu_baseline": {"value": value, "unit": "outer_it/s", "cores": samples["cores"],
-                             "kind": samples["kind"], "sample": samples["sample"]},
-            "e2e": {"value": value, "unit": "outer_it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "wall_s": el}
+            "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded NumPy slabs of the C5 workload)",
+            "config": workload_config(args.gpus),
+            "cpu_baseline": {"value": value, "unit": "outer_it/s", "cores": threads, "kind": kind,
+                             "sample": f"per step: {threads} host threads, each one J-CoMM outer iteration "
+                                       f"(L=5, beta=0.5, R=64) of the compiled reference on its own "
+                                       f"{'x'.join(map(str, REF_SAMPLE_DIMS))} slab of C5 (1/{int(1/frac)} of "
+                                       f"the entries); value = threads x fraction / step wall time"},
+            "e2e": {"value": value, "unit": "outer_it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
@@ -422,79 +515,67 @@ def run_reference(args, rank_id):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
-    ap.add_argument("--no-c4", dest="c4", action="store_false", help="skip the sparse C4 side measurement")
-    ap.add_argument("--no-c5", dest="c5", action="store_false", help="skip the large dense C5 side measurement")
-    ap.add_argument("--c5-steps", type=int, default=2, help="timed C5 outer iterations (each ~0.2 s on one B200)")
+    ap.add_argument("--no-side", dest="side", action="store_false", help="skip the C1-C4 side measurements")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank_id = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-
+    d = Dist()
     if args.impl == "reference":
-        run_reference(args, rank_id)
+        run_reference(args, d)
         return
+    args.warmup = max(args.warmup, 3)
+    d.init()
 
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    c5 = run_c5(args, d)
+    sides = {}
+    if args.side:
+        sides["c2"] = side(run_c2, args, d)
+        if d.world == 1:
+            sides["c1"] = side(run_c1, args, d)
+            sides["c3"] = side(run_c3, args, d)
+            sides["c4_sparse"] = side(run_c4, args, d)
 
-    per_beta, launches, pst, clocks, e2e, c4, c5 = run_ours(args, rank_id, world, local_rank)
-
-    if rank_id == 0:
-        E = int(np.prod(DIMS))
+    if d.rank == 0:
+        E = float(np.prod(C5_DIMS))
         peak, peak_src = peaks()
-        # dominant kernel: K3 contraction pass (15 of the 16 streaming passes per outer)
-        avg_ms = pst["contract_ms"] / max(1, pst["contract_launches"])
-        ebytes = E * 2 * 4 // world  # P~ and Q~ fp32 read once per launch (beta != 1)
-        achieved = ebytes / (avg_ms * 1e-3) / 1e9
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_contract_traffic.json")
-        if os.path.exists(tp):
-            with open(tp) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
-        fma_rate = (E // world) * 2 * RANK / (avg_ms * 1e-3) / 1e12
-        head = per_beta[HEADLINE_BETA]
+        pst = c5["pst"]
+        # dominant kernel: K3 tensor-core contraction (20 of the 21 streaming passes per outer)
+        k3_ms = pst["contract_ms"] / max(1, pst["contract_launches"])
+        k3_bytes = 8.0 * c5["local_entries"]  # P~ and Q~ (bf16 hi+lo planes, 4 B each) read once per launch
+        achieved = k3_bytes / (k3_ms * 1e-3) / 1e9
+        traffic, traffic_src = ncu_traffic("c5_k3")
+        alg = 4.0 * c5["local_entries"] * (1 + 2 + 2 * C5_INNER * 4)  # X once; P~/Q~ written once, read 20x
+        ms_step = c5["ms"] / args.steps
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            try:
-                cpu = cpu_sample(2)
-            except Exception as ex:  # the baseline must never sink the bench line
-                cpu = {"value": None, "unit": "outer_it/s", "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+        if d.world == 1 and not args.no_cpu_baseline:
+            cpu = side(cpu_baseline)
         line = {
-            "metric": METRIC, "value": head["outer_it_per_s"], "unit": "outer_it/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "metric": METRIC, "value": args.steps / (c5["ms"] * 1e-3), "unit": "outer_it/s", "n_gpus": d.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded GPU generator: U[0,1) CP truth x Gamma(10,0.1); init U[0.1,1.1))",
-            "config": {"workload": "C2: dense CP 512x512x512 fp32, R=32, J-CoMM L=5, beta=0.5 headline",
-                       "global_batch": 1, "seq_len": 0, "parallelism": f"mode-0 slabs dp{world}",
-                       "l2": "inputs (X 0.5 GB, P~/Q~ 1 GB) exceed L2; no flush"},
-            "per_beta": {str(b): v for b, v in per_beta.items()},
-            "roofline": {"bound": "hbm", "kernel": "tc_contract_kernel (K3 J-CoMM inner pass, tcgen05)",
+            "data": "synthetic (seeded on-device Philox generator: U[0,1) CP truth x Gamma(10,0.1); init U[0.1,1.1))",
+            "config": workload_config(d.world),
+            "roofline": {"bound": "hbm", "kernel": "tc_contract_kernel<64> (K3 J-CoMM inner contraction, tcgen05)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "peak_source": peak_src, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": ebytes, "avg_launch_ms": avg_ms,
-                         "fma_rate_tflops_equiv": fma_rate, "fma_frac": fma_rate / FFMA_PEAK_T},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "c4_sparse": c4,
-            "c5_large": c5,
-            "kernel_breakdown_ms_per_step": {
-                "recon": pst["recon_ms"] / max(1, min(args.steps, 5)),
-                "contract": pst["contract_ms"] / max(1, min(args.steps, 5)),
-                "other": (pst["device_ms"] - pst["recon_ms"] - pst["contract_ms"]) / max(1, min(args.steps, 5))},
+                         "peak_source": peak_src, "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": k3_bytes, "avg_launch_ms": k3_ms,
+                         "per_unit": "8 B per tensor entry per launch (P~ and Q~ as bf16 hi/lo planes)"},
+            "whole_step": {"algorithmic_bytes": alg, "GBps": alg / (ms_step * 1e-3) / 1e9,
+                           "frac_of_peak": alg / (ms_step * 1e-3) / 1e9 / peak,
+                           "kernel_ms_one_eager_outer": {"recon": pst["recon_ms"], "contract": pst["contract_ms"],
+                                                         "other": pst["device_ms"] - pst["recon_ms"]
+                                                         - pst["contract_ms"]}},
+            "cpu_baseline": cpu, "e2e": c5["e2e"], "gpu_launches": c5["launches"], "clocks": c5["clocks"],
+            "final_loss": c5["final_loss"],
         }
+        line.update(sides)
         print(json.dumps(line))
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
+    if d.dist is not None:
+        d.dist.barrier()
+        d.dist.destroy_process_group()
 
 
 if __name__ == "__main__":

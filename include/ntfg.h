@@ -118,6 +118,15 @@ ntfg_status ntfg_context_set_profiling(ntfg_context* ctx, int enabled);
 ntfg_status ntfg_context_set_comm_buffer(ntfg_context* ctx, double* device_buf, size_t capacity);
 /* Release cached device buffers. */
 ntfg_status ntfg_context_trim(ntfg_context* ctx);
+/* Native data-parallel communicator (new; SURVEY.md 8(e) -- the reference is
+ * single-process, so there is no reference interface to replace).  Rank 0
+ * creates a 128-byte id (ncclGetUniqueId), the caller broadcasts it, then
+ * every rank attaches it to its context (ncclCommInitRank on ctx's device).
+ * Sharded fits then allreduce their packed fp64 partials with ncclAllReduce on
+ * the context stream, inside the captured outer-iteration CUDA graph, and the
+ * allreduce hook is not used.  libnccl.so.2 is resolved at run time. */
+ntfg_status ntfg_nccl_unique_id(void* id_out);
+ntfg_status ntfg_context_init_nccl(ntfg_context* ctx, const void* id, int32_t nranks, int32_t rank);
 
 /* validate_fit_config (reference config.hpp:43, config.cpp:7-18) */
 ntfg_status ntfg_validate_fit_config(const ntfg_fit_config* cfg);

@@ -77,6 +77,8 @@ _SIGS = {
     "ntfg_context_trim": [_V],
     "ntfg_context_set_profiling": [_V, C.c_int],
     "ntfg_context_set_comm_buffer": [_V, _V, C.c_size_t],
+    "ntfg_nccl_unique_id": [_V],
+    "ntfg_context_init_nccl": [_V, _V, C.c_int32, C.c_int32],
     "ntfg_validate_fit_config": [C.POINTER(FitConfigC)],
     "ntfg_cp_fit": [_V, C.POINTER(FitConfigC), C.c_int32, C.c_uint32, _U, _V, C.c_int32, C.c_int32,
                     C.POINTER(ShardC), _P, C.POINTER(TraceRowC), _U],

@@ -221,12 +221,27 @@ class Context:
     def set_comm_buffer(self, ptr: int, capacity: int):
         _check(N.load().ntfg_context_set_comm_buffer(self.h, C.c_void_p(ptr), int(capacity)))
 
+    def init_nccl(self, unique_id: bytes, nranks: int, rank: int):
+        """Attach a native NCCL communicator (ntfg_context_init_nccl): sharded
+        fits then allreduce on the context stream inside the CUDA graph."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(N.load().ntfg_context_init_nccl(self.h, C.cast(buf, C.c_void_p), int(nranks), int(rank)))
+
     def trim(self):
         _check(N.load().ntfg_context_trim(self.h))
 
 
 _default = {}
 _dlock = threading.Lock()
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through libntfg (rank 0 creates it, the caller broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    _check(N.load().ntfg_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return buf.raw
 
 
 def default_context(device: int = 0) -> Context:
@@ -288,6 +303,10 @@ def _x_arg(x):
             if x.dtype not in (torch.float32, torch.float64):
                 raise ShapeError("x must be float32 or float64")
             loc = 1 if x.is_cuda else 0
+            if x.is_cuda:
+                # the engine reads X on its own stream: finish torch's pending
+                # writes to it first (no cross-stream race on device inputs)
+                torch.cuda.current_stream(x.device).synchronize()
             return (list(x.shape), C.c_void_p(x.data_ptr()), 1 if x.dtype == torch.float32 else 0,
                     loc, x)
     except ImportError:

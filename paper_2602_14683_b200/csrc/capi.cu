@@ -5,6 +5,7 @@
 #include <string>
 
 #include "engine.cuh"
+#include "nccl_comm.cuh"
 
 namespace ntfg {
 // cp_api.cu
@@ -139,6 +140,7 @@ NTFG_API ntfg_status ntfg_context_destroy(ntfg_context* ctx) {
     ctx->activate();
     cudaStreamSynchronize(ctx->stream);
     ctx->bufs.release();
+    if (ctx->nccl) ntfg::nccl_comm_destroy(ctx->nccl);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -173,6 +175,26 @@ NTFG_API ntfg_status ntfg_context_set_comm_buffer(ntfg_context* ctx, double* buf
   return with_ctx(ctx, [&](ntfg::Context& c) {
     c.comm_buf = buf;
     c.comm_cap = buf ? cap : 0;
+  });
+}
+
+NTFG_API ntfg_status ntfg_nccl_unique_id(void* id_out) {
+  return guard([&] {
+    need(id_out, "id_out");
+    ntfg::nccl_unique_id(id_out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_context_init_nccl(ntfg_context* ctx, const void* id, int32_t nranks, int32_t rank) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(id, "id");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw ntfg::Error(NTFG_ERR_DOMAIN, "invalid nranks/rank");
+    if (c.nccl) {
+      ntfg::nccl_comm_destroy(c.nccl);
+      c.nccl = nullptr;
+    }
+    c.nccl = ntfg::nccl_comm_init(id, nranks, rank);
+    c.nccl_ranks = nranks;
   });
 }
 

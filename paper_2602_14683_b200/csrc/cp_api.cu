@@ -54,7 +54,7 @@ std::vector<ntfg_trace_row> cp_fit_t(Context& c, const ntfg_fit_config& cfg, int
   if (cfg.extrapolate) {
     // BMMe (reference cp.cpp:249-263 / 276-292): prev = init, t_0 = 1
     double* prev = c.buf<double>("cp.prev", F);
-    double* alpha = c.buf<double>("cp.alpha", 1);
+    double* alpha = c.buf<double>("cp.alpha", 3);  // [alpha | norm^2 shard | rest]
     int* iter = c.buf<int>("cp.iter", 1);
     const auto an = nesterov_alphas(cfg.max_iters);
     double* alpha_nes = c.buf<double>("cp.alpha_nes", an.size());
@@ -63,8 +63,13 @@ std::vector<ntfg_trace_row> cp_fit_t(Context& c, const ntfg_fit_config& cfg, int
     NTFG_CUDA(cudaMemsetAsync(iter, 0, sizeof(int), c.stream));
     c.sync();  // alpha_nes host vector goes out of scope
     h.body = [&e, &c, &cfg, prev, alpha, iter, alpha_nes, F, bytes, algo, L]() {
-      extrap_alpha_kernel<<<1, 256, 0, c.stream>>>(e.A_all(), prev, int64_t(F), alpha_nes, iter,
-                                                   cfg.extrap_cap, cfg.extrap_delta, alpha);
+      // mode-0 rows [0, I0_local * R) are this rank's shard when data-parallel
+      const int64_t s1 = e.sharded() ? e.offset(1) : 0;
+      extrap_norm_kernel<<<1, 256, 0, c.stream>>>(e.A_all(), prev, int64_t(F), 0, s1, alpha + 1);
+      NTFG_LAUNCHED(c);
+      if (e.sharded()) e.allreduce(alpha + 1, 1);
+      extrap_alpha_finish_kernel<<<1, 1, 0, c.stream>>>(alpha + 1, alpha_nes, iter, cfg.extrap_cap,
+                                                        cfg.extrap_delta, alpha);
       NTFG_LAUNCHED(c);
       extrap_apply_kernel<<<int(ceil_div(int64_t(F), 256)), 256, 0, c.stream>>>(
           e.A_all(), prev, int64_t(F), alpha, cfg.eps, e.anchors());

@@ -18,6 +18,7 @@
 #include "coo_kernels.cuh"
 #include "cp_kernels.cuh"
 #include "engine.cuh"
+#include "nccl_comm.cuh"
 #include "stream3_kernels.cuh"
 #include "recon_tile.cuh"
 #include "tc_contract.cuh"
@@ -58,7 +59,7 @@ class CpEngine {
       if (shard->slab_begin + dims[0] > shard->global_dim0)
         throw Error(NTFG_ERR_SHAPE, "shard slab exceeds the global mode-0 extent");
       E_global_ = E_ / g_.dims[0] * int64_t(shard->global_dim0);
-      sharded_ = c_.allreduce != nullptr;
+      sharded_ = c_.has_comm();
     }
     off_.resize(N_ + 1, 0);
     for (int m = 0; m < N_; ++m) off_[m + 1] = off_[m] + g_.dims[m] * R_;
@@ -363,6 +364,34 @@ class CpEngine {
   void disable_tc() { tc_allowed_ = false; tc_ = false; }
   void* plane(int i) { ensure_pq(); return planes_[i]; }
 
+  // work split of one tensor-core contraction: case A (last mode) = row
+  // chunks, case B = (target index, split) pairs; chunk = rows per unit
+  static int64_t tc_unit_rows_cap() {  // experiments: NTFG_TC_UNIT_ROWS caps the TMEM accumulation length
+    static const int64_t v = [] { const char* e = std::getenv("NTFG_TC_UNIT_ROWS"); return e ? std::atoll(e) : 0; }();
+    return v;
+  }
+  void tc_units(int n, int64_t& units, int64_t& S, int64_t& chunk) const {
+    const int64_t cap = tc_unit_rows_cap();
+    if (n == N_ - 1) {
+      const int64_t target = std::min<int64_t>(ceil_div(g_.rows, kTcRows), int64_t(c_.sm_count));
+      chunk = ceil_div(ceil_div(g_.rows, target), kTcRows) * kTcRows;
+      if (cap > 0) chunk = std::min(chunk, ceil_div(cap, kTcRows) * kTcRows);
+      units = ceil_div(g_.rows, chunk);
+      S = 1;
+      return;
+    }
+    const int64_t In = g_.dims[n];
+    int64_t An = 1, Bn = 1;
+    for (int m = 0; m < n; ++m) An *= g_.dims[m];
+    for (int m = n + 1; m < N_ - 1; ++m) Bn *= g_.dims[m];
+    const int64_t tot = An * Bn;
+    int64_t S0 = std::max<int64_t>(1, std::min<int64_t>(ceil_div(int64_t(4) * c_.sm_count, In), ceil_div(tot, kTcRows)));
+    if (cap > 0) S0 = std::max(S0, ceil_div(tot, ceil_div(cap, kTcRows) * kTcRows));
+    chunk = ceil_div(ceil_div(tot, S0), kTcRows) * kTcRows;
+    S = ceil_div(tot, chunk);
+    units = In * S;
+  }
+
   void tc_contract(int n, int ns, const Stream* st, int64_t& units_out, int64_t& S_out) {
     const bool caseA = (n == N_ - 1);
     TcParams p{};
@@ -378,10 +407,7 @@ class CpEngine {
     TcMaps maps{};
     int64_t mapB, mapI = 1, mapA = 1;
     if (caseA) {
-      const int64_t target = std::min<int64_t>(ceil_div(g_.rows, kTcRows), int64_t(c_.sm_count));
-      p.chunk = ceil_div(ceil_div(g_.rows, target), kTcRows) * kTcRows;
-      p.units = ceil_div(g_.rows, p.chunk);
-      p.S = 1;
+      tc_units(n, p.units, p.S, p.chunk);
       p.An = 1;
       p.Bn = g_.rows;
       p.boxB = kTcRows;
@@ -391,12 +417,7 @@ class CpEngine {
       int64_t An = 1, Bn = 1;
       for (int m = 0; m < n; ++m) An *= g_.dims[m];
       for (int m = n + 1; m < N_ - 1; ++m) Bn *= g_.dims[m];
-      const int64_t tot = An * Bn;
-      const int64_t S = std::max<int64_t>(1, std::min<int64_t>(ceil_div(int64_t(4) * c_.sm_count, In),
-                                                               ceil_div(tot, kTcRows)));
-      p.chunk = ceil_div(ceil_div(tot, S), kTcRows) * kTcRows;
-      p.S = ceil_div(tot, p.chunk);
-      p.units = In * p.S;
+      tc_units(n, p.units, p.S, p.chunk);
       p.An = An;
       p.Bn = Bn;
       p.boxB = int(Bn >= kTcRows ? kTcRows : Bn);
@@ -533,6 +554,13 @@ class CpEngine {
         else b = std::max(b, size_t(ns) * pl.In * pl.S * RP_);
       }
     }
+    if (tc_)
+      for (int n = 0; n < N_; ++n) {
+        int64_t units, S, chunk;
+        tc_units(n, units, S, chunk);
+        if (n == N_ - 1) a = std::max(a, size_t(ns) * units * g_.K * RP_);
+        else b = std::max(b, size_t(ns) * units * RP_);
+      }
     partA_ = c_.buf<T>("cp.partA", std::max<size_t>(a, 1));
     partB_ = c_.buf<double>("cp.partB", std::max<size_t>(b, 1));
     partAd_ = c_.buf<double>("cp.partAd", std::max<size_t>(a / 8 + size_t(ns) * g_.K * RP_, 1));
@@ -1019,6 +1047,10 @@ class CpEngine {
   }
 
   void allreduce(double* buf, size_t count) {
+    if (c_.nccl) {  // in place on the engine stream; graph-capturable
+      nccl_allreduce_sum(c_.nccl, buf, count, c_.stream);
+      return;
+    }
     if (!c_.allreduce) return;
     double* target = buf;
     if (c_.comm_buf) {

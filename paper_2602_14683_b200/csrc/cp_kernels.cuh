@@ -415,28 +415,44 @@ static __global__ void chi_all_kernel(const double* z, const double* zref, int64
 
 // ---- BMMe extrapolation (reference cp.cpp:137-198, tucker.cpp:151-217) ----
 // alpha = min(alpha_nes[it], cap / (||[cur - prev]_+||_F + delta)); it = (*iter)++
-static __global__ void extrap_alpha_kernel(const double* cur, const double* prev, int64_t n,
-                                    const double* alpha_nes, int* iter, double cap, double delta,
-                                    double* alpha_out) {
-  __shared__ double red[256];
-  double s = 0.0;
+// The squared norm is split into the entries of the sharded range [s0, s1)
+// (the mode-0 factor rows this rank owns in a data-parallel fit) and the
+// replicated rest, so a sharded fit allreduces part[0] before finishing and
+// every rank computes the same alpha over the WHOLE model (cp.cpp:178-194).
+static __global__ void extrap_norm_kernel(const double* cur, const double* prev, int64_t n, int64_t s0,
+                                          int64_t s1, double* part) {
+  __shared__ double red[2][256];
+  double a = 0.0, b = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const double d = cur[i] - prev[i];
-    if (d > 0.0) s += d * d;
+    if (d > 0.0) {
+      if (i >= s0 && i < s1) a += d * d;
+      else b += d * d;
+    }
   }
-  red[threadIdx.x] = s;
+  red[0][threadIdx.x] = a;
+  red[1][threadIdx.x] = b;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+    if (int(threadIdx.x) < w) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + w];
+      red[1][threadIdx.x] += red[1][threadIdx.x + w];
+    }
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    const int it = *iter;
-    const double a = cap / (sqrt(red[0]) + delta);
-    const double an = alpha_nes[it];
-    *alpha_out = an < a ? an : a;  // std::min(alpha_nes, cap / (...))
-    *iter = it + 1;
+    part[0] = red[0][0];
+    part[1] = red[1][0];
   }
+}
+
+static __global__ void extrap_alpha_finish_kernel(const double* part, const double* alpha_nes, int* iter,
+                                                  double cap, double delta, double* alpha_out) {
+  const int it = *iter;
+  const double a = cap / (sqrt(part[0] + part[1]) + delta);
+  const double an = alpha_nes[it];
+  *alpha_out = an < a ? an : a;  // std::min(alpha_nes, cap / (...))
+  *iter = it + 1;
 }
 
 // out = max(cur + alpha [cur - prev]_+, eps)

@@ -84,6 +84,9 @@ struct Context {
   bool profile = false;
   double* comm_buf = nullptr;
   size_t comm_cap = 0;
+  void* nccl = nullptr;  // native communicator (nccl_comm.cuh); preferred over the hook
+  int nccl_ranks = 0;
+  bool has_comm() const { return allreduce != nullptr || nccl != nullptr; }
   BufferCache bufs;
   PinnedCache pinned;
   int sm_count = 148;

@@ -36,7 +36,9 @@ inline std::vector<ntfg_trace_row> run_fit_loop(Context& c, const ntfg_fit_confi
                                                 unsigned* flags_dev) {
   const uint64_t K = cfg.max_iters;
   const bool check_each = cfg.tol > 0.0;
-  const bool graphs = cfg.use_graphs && c.allreduce == nullptr && !c.profile;
+  // the Python/host hook cannot run inside a graph; the native NCCL
+  // communicator can (ncclAllReduce is stream-ordered and capturable)
+  const bool graphs = cfg.use_graphs && (c.allreduce == nullptr || c.nccl != nullptr) && !c.profile;
   std::vector<ntfg_trace_row> trace;
   double* hl = static_cast<double*>(c.pinned.get((K + 2) * sizeof(double)));
 

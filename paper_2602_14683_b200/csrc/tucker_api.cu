@@ -60,7 +60,7 @@ std::vector<ntfg_trace_row> tucker_fit_t(Context& c, const ntfg_fit_config& cfg,
   h.objective = [&]() { e.objective(); };
   if (cfg.extrapolate) {
     double* prev = c.buf<double>("tk.prev", B);
-    double* alpha = c.buf<double>("tk.alpha", 1);
+    double* alpha = c.buf<double>("tk.alpha", 3);  // [alpha | norm^2 shard | rest]
     int* iter = c.buf<int>("tk.iter", 1);
     const auto an = nesterov_alphas_t(cfg.max_iters);
     double* alpha_nes = c.buf<double>("tk.alpha_nes", an.size());
@@ -69,8 +69,15 @@ std::vector<ntfg_trace_row> tucker_fit_t(Context& c, const ntfg_fit_config& cfg,
     NTFG_CUDA(cudaMemsetAsync(iter, 0, sizeof(int), c.stream));
     c.sync();
     h.body = [&e, &c, &cfg, prev, alpha, iter, alpha_nes, B, bytes, algo, L]() {
-      extrap_alpha_kernel<<<1, 256, 0, c.stream>>>(e.model(), prev, int64_t(B), alpha_nes, iter,
-                                                   cfg.extrap_cap, cfg.extrap_delta, alpha);
+      // [core | A_0 | A_1 ...]: A_0's rows are this rank's shard when data-parallel
+      const bool sh = e.stream().sharded();
+      const int64_t s0 = sh ? e.core_size() : 0;
+      const int64_t s1 = sh ? e.core_size() + e.factor_offset(1) : 0;
+      extrap_norm_kernel<<<1, 256, 0, c.stream>>>(e.model(), prev, int64_t(B), s0, s1, alpha + 1);
+      NTFG_LAUNCHED(c);
+      if (sh) e.stream().allreduce(alpha + 1, 1);
+      extrap_alpha_finish_kernel<<<1, 1, 0, c.stream>>>(alpha + 1, alpha_nes, iter, cfg.extrap_cap,
+                                                        cfg.extrap_delta, alpha);
       NTFG_LAUNCHED(c);
       extrap_apply_kernel<<<int(ceil_div(int64_t(B), 256)), 256, 0, c.stream>>>(
           e.model(), prev, int64_t(B), alpha, cfg.eps, e.anchors());

@@ -70,7 +70,7 @@ class TuckerEngine {
     W2_ = c_.buf<double>("tk.W2", size_t(big));
     int64_t nb = Jtot_;
     for (int m = 0; m < N_; ++m) nb = std::max(nb, I_[m] * J_[m]);
-    num_ = c_.buf<double>("tk.num", size_t(nb));
+    num_ = c_.buf<double>("tk.num", size_t(2 * nb));  // [Num | Den] packed for the allreduce
     den_ = c_.buf<double>("tk.den", size_t(nb));
   }
 
@@ -188,6 +188,18 @@ class TuckerEngine {
     c_.prof_end(ph);
   }
 
+  // Data-parallel (mode-0 slabs): the core's and factors
+  // 1..L-1's Num/Den are sums over the WHOLE tensor (tucker.cpp:44-88), so
+  // each rank's slab-local sums are packed [Num | Den] and allreduced before
+  // the identical MU step on every rank.  Factor 0's rows are rank-local;
+  // the last factor reduces inside CpEngine::contract_and_update.
+  void reduce_numden(int64_t cnt) {
+    if (!s_.sharded()) return;
+    c_.d2d(num_ + cnt, den_, size_t(cnt) * sizeof(double));
+    s_.allreduce(num_, size_t(2 * cnt));
+    c_.d2d(den_, num_ + cnt, size_t(cnt) * sizeof(double));
+  }
+
   void mu_dense(const double* anchor, int64_t n, double* out, const double* ref, double* c1,
                 double* c2) {
     mu_dense_kernel<<<int(ceil_div(n, 256)), 256, 0, c_.stream>>>(anchor, num_, den_, n, gamma_, eps_, beta_, out,
@@ -230,6 +242,7 @@ class TuckerEngine {
     recon(anchor_core, fac, stageL_, true, objective);
     contract_core(s_.p(), fac, num_);
     contract_core(s_.q_always(), fac, den_);
+    reduce_numden(Jtot_);
     mu_dense(anchor_core, Jtot_, G(), nullptr, nullptr, nullptr);
   }
 
@@ -247,6 +260,7 @@ class TuckerEngine {
     } else {
       contract_factor(s_.p(), G(), fac, n, num_);
       contract_factor(s_.q_always(), G(), fac, n, den_);
+      if (n != 0) reduce_numden(I_[n] * J_[n]);
       mu_dense(anchor, I_[n] * J_[n], A(n), nullptr, nullptr, nullptr);
     }
   }
@@ -283,6 +297,7 @@ class TuckerEngine {
     fac_ptrs(chi2_, f2);
     contract_core(s_.p(), f1, num_);
     contract_core(s_.q_always(), f2, den_);
+    reduce_numden(Jtot_);
     mu_dense(ref_, Jtot_, G(), ref_, chi1_, chi2_);
   }
 
@@ -297,6 +312,7 @@ class TuckerEngine {
     } else {
       contract_factor(s_.p(), chi1_, f1, n, num_);
       contract_factor(s_.q_always(), chi2_, f2, n, den_);
+      if (n != 0) reduce_numden(I_[n] * J_[n]);
       mu_dense(ref_ + o, I_[n] * J_[n], A(n), ref_ + o, chi1_ + o, chi2_ + o);
     }
   }

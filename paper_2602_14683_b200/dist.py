@@ -35,22 +35,55 @@ def shard_model(init: Sequence[np.ndarray], row0: int, row1: int) -> List[np.nda
 
 
 def make_allreduce(comm, group=None):
-    """Returns fn(ptr, count, stream) summing comm[:count] across the group."""
+    """Returns fn(ptr, count, stream) summing comm[:count] across the group.
+
+    The engine enqueues the copy into ``comm`` on ITS stream and then calls the
+    hook; the collective is issued on that same stream (ExternalStream), so it
+    is ordered after the copy-in and before the engine's copy-back.  CUDA
+    buffers with a CPU-only backend (gloo) go through host memory."""
+    import torch
     import torch.distributed as dist
 
     def allreduce(ptr, count, stream):
-        dist.all_reduce(comm[:count], op=dist.ReduceOp.SUM, group=group)
+        dev = comm.device
+        if dev.type == "cuda":
+            s = torch.cuda.ExternalStream(stream, device=dev) if stream else torch.cuda.current_stream(dev)
+            with torch.cuda.stream(s):
+                if dist.get_backend(group) == "gloo":
+                    s.synchronize()
+                    host = comm[:count].cpu()
+                    dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+                    comm[:count].copy_(host)
+                else:
+                    dist.all_reduce(comm[:count], op=dist.ReduceOp.SUM, group=group)
+        else:
+            dist.all_reduce(comm[:count], op=dist.ReduceOp.SUM, group=group)
 
     return allreduce
 
 
 def attach(ctx, device, capacity: int, group=None):
-    """Registers the comm buffer + hook on an ntf Context; returns the buffer."""
+    """Registers the comm buffer + Python hook on an ntf Context; returns the
+    buffer.  Works with any torch.distributed backend; graphs are off while a
+    hook is set (see attach_nccl for the native path)."""
     import torch
     comm = torch.zeros(int(capacity), dtype=torch.float64, device=device)
     ctx.set_comm_buffer(comm.data_ptr(), comm.numel())
     ctx.set_allreduce(make_allreduce(comm, group))
     return comm
+
+
+def attach_nccl(ctx, group=None):
+    """Native path: rank 0 of ``group`` creates an NCCL unique id, it is
+    broadcast over torch.distributed, and every rank attaches a communicator
+    to its context (ntfg_context_init_nccl).  The engine then allreduces with
+    ncclAllReduce on its own stream, inside the captured CUDA graph -- no
+    Python runs per block update."""
+    import torch.distributed as dist
+    from . import api
+    obj = [api.nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    ctx.init_nccl(obj[0], dist.get_world_size(group), dist.get_rank(group))
 
 
 def gather_mode0(local: np.ndarray, global_dim0: int, group=None) -> np.ndarray:
