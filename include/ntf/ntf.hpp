@@ -194,6 +194,24 @@ CpFactors jcomm_outer_step(const CpFactors& f, const DenseTensor& x, const BetaP
                            std::size_t inner_steps, double eps);
 CpFitResult jcomm_fit(const DenseTensor& x, CpFactors init, const FitConfig& cfg);
 
+/// BMMe step-level API (reference cp.hpp:80-110).  Factor-sized host
+/// arithmetic, as in the reference; the fit drivers run the same scheme on
+/// the device (extrap_norm / extrap_apply kernels).
+struct ExtrapolationState {
+    CpFactors previous;
+    double t = 1.0;
+    double alpha = 0.0;
+    double cap = 1.0;
+    double delta = 1e-6;
+    double eps = 1e-12;
+    bool enabled = false;
+};
+ExtrapolationState make_extrapolation_state(const CpFactors& initial, bool enabled, double cap, double delta,
+                                            double eps);
+void extrapolation_begin_iteration(ExtrapolationState& st, const CpFactors& current);
+Matrix extrapolate_block(const Matrix& current, const ExtrapolationState& st, std::size_t block);
+void extrapolation_end_iteration(ExtrapolationState& st, const CpFactors& iterate);
+
 // ---- Tucker (reference tucker.hpp, tensor.hpp contractions) -------------------------------
 struct TuckerModel {
     DenseTensor core;
@@ -227,11 +245,13 @@ TuckerModel block_factor_update_anchored(const TuckerModel& m, std::size_t mode,
 TuckerModel tucker_bcomm_sweep(const TuckerModel& m, const DenseTensor& x, const BetaParam& p, double eps);
 TuckerFitResult tucker_bcomm_fit(const DenseTensor& x, TuckerModel init, const FitConfig& cfg);
 
-/// The device engine rebuilds P~/Q~ from (ref, x) inside each inner call, so
-/// the cache holds the data instead of host copies of P~/Q~.
+/// Reference tucker.hpp:59-63: the reference model plus host copies of its
+/// P~/Q~ (computed on the device by make_jcomm_tucker_reference and uploaded
+/// again by the inner updates, like the CP JcommCpReference).
 struct JcommTuckerReference {
     TuckerModel ref;
-    DenseTensor x;
+    DenseTensor p;
+    DenseTensor q;
 };
 JcommTuckerReference make_jcomm_tucker_reference(const TuckerModel& ref, const DenseTensor& x,
                                                  const BetaParam& p, double eps);
@@ -242,5 +262,22 @@ TuckerModel jcomm_inner_factor_update(const TuckerModel& current, const JcommTuc
 TuckerModel jcomm_tucker_outer_step(const TuckerModel& m, const DenseTensor& x, const BetaParam& p,
                                     std::size_t inner_steps, double eps);
 TuckerFitResult tucker_jcomm_fit(const DenseTensor& x, TuckerModel init, const FitConfig& cfg);
+
+/// reference tucker.hpp:88-106: block 0 is the core, block n+1 is factor n.
+struct TuckerExtrapolationState {
+    TuckerModel previous;
+    double t = 1.0;
+    double alpha = 0.0;
+    double cap = 1.0;
+    double delta = 1e-6;
+    double eps = 1e-12;
+    bool enabled = false;
+};
+TuckerExtrapolationState make_tucker_extrapolation_state(const TuckerModel& initial, bool enabled, double cap,
+                                                         double delta, double eps);
+void extrapolation_begin_iteration(TuckerExtrapolationState& st, const TuckerModel& current);
+DenseTensor extrapolate_core(const DenseTensor& current, const TuckerExtrapolationState& st);
+Matrix extrapolate_block(const Matrix& current, const TuckerExtrapolationState& st, std::size_t mode);
+void extrapolation_end_iteration(TuckerExtrapolationState& st, const TuckerModel& iterate);
 
 }  // namespace ntf

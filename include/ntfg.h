@@ -150,8 +150,13 @@ ntfg_status ntfg_cp_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t a
 ntfg_status ntfg_cp_fit_coo(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t algo,
                             uint32_t order, const uint64_t* dims, uint64_t nnz,
                             const int32_t* indices, const void* values, int32_t values_dtype,
-                            int32_t location, double* factors_inout, ntfg_trace_row* trace,
-                            uint64_t* trace_len);
+                            int32_t location, const ntfg_shard* shard, double* factors_inout,
+                            ntfg_trace_row* trace, uint64_t* trace_len);
+/* Data-parallel sparse fits (shard != NULL): the nonzeros are
+ * partitioned by mode-0 index ranges; each rank passes the nonzeros of its
+ * slab with i_0 rebased to the slab (dims[0] = slab rows) and its A_0 rows,
+ * exactly like a dense slab.  Mode-0 numerators stay local; modes >= 1, the
+ * mode-0 column sums and the objective's nonzero part are allreduced. */
 
 /* MU-unfold baseline (reference unfold.hpp:35-37, unfold.cpp:109-135,187-197):
  * explicit Khatri-Rao + unfolding + cuBLAS GEMMs; the comparison path for the
@@ -293,6 +298,21 @@ ntfg_status ntfg_tucker_step(ntfg_context* ctx, int32_t precision, int32_t kind,
                              const uint64_t* dims, const double* x, const uint64_t* ranks,
                              const double* ref_core, const double* ref_factors,
                              double* core_inout, double* factors_inout, uint32_t mode);
+
+/* make_jcomm_tucker_reference (reference tucker.hpp:59-67, tucker.cpp:92-98):
+ * P~ and Q~ (E fp64 each, host) of the reference model (ref_core, ref_factors). */
+ntfg_status ntfg_tucker_jcomm_reference(ntfg_context* ctx, int32_t precision, double beta, double eps,
+                                        uint32_t order, const uint64_t* dims, const double* x,
+                                        const uint64_t* ranks, const double* ref_core,
+                                        const double* ref_factors, double* p_out, double* q_out);
+/* jcomm_inner_core_update (block = -1) / jcomm_inner_factor_update (block =
+ * mode) from the cached host P~/Q~ (reference tucker.hpp:69-78,
+ * tucker.cpp:100-149): current model in/out, anchored at the reference. */
+ntfg_status ntfg_tucker_jcomm_inner_update(ntfg_context* ctx, int32_t precision, double beta, double eps,
+                                           uint32_t order, const uint64_t* dims, const double* p,
+                                           const double* q, const uint64_t* ranks, const double* ref_core,
+                                           const double* ref_factors, double* core_inout,
+                                           double* factors_inout, int32_t block);
 
 #ifdef __cplusplus
 }

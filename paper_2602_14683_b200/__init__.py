@@ -13,6 +13,8 @@ from .api import (  # noqa: F401
     jcomm_inner_update, jcomm_outer_step, jcomm_tucker_outer_step, make_jcomm_reference,
     make_jcomm_tucker_reference, mu_unfold_cp_fit, mu_unfold_cp_sweep, mu_unfold_tucker_fit, mu_unfold_tucker_sweep, tucker_bcomm_fit, tucker_bcomm_sweep, tucker_factor_contract,
     tucker_jcomm_fit, tucker_multimode_contract, tucker_objective, tucker_reconstruct,
-    nccl_unique_id, validate_fit_config)
+    nccl_unique_id, validate_fit_config, ExtrapolationState, make_extrapolation_state,
+    make_tucker_extrapolation_state, extrapolation_begin_iteration, extrapolate_block, extrapolate_core,
+    extrapolation_end_iteration)
 
 __version__ = "0.1.0"

@@ -83,7 +83,7 @@ _SIGS = {
     "ntfg_cp_fit": [_V, C.POINTER(FitConfigC), C.c_int32, C.c_uint32, _U, _V, C.c_int32, C.c_int32,
                     C.POINTER(ShardC), _P, C.POINTER(TraceRowC), _U],
     "ntfg_cp_fit_coo": [_V, C.POINTER(FitConfigC), C.c_int32, C.c_uint32, _U, C.c_uint64, _V, _V, C.c_int32,
-                        C.c_int32, _P, C.POINTER(TraceRowC), _U],
+                        C.c_int32, C.POINTER(ShardC), _P, C.POINTER(TraceRowC), _U],
     "ntfg_cp_mu_unfold_fit": [_V, C.POINTER(FitConfigC), C.c_uint32, _U, _V, C.c_int32, C.c_int32, _P,
                               C.POINTER(TraceRowC), _U],
     "ntfg_cp_mu_unfold_sweep": [_V, C.c_int32, C.c_double, C.c_double, C.c_uint32, _U, _P, C.c_uint64, _P],
@@ -119,6 +119,10 @@ _SIGS = {
     "ntfg_tucker_multimode_contract": [_V, C.c_int32, C.c_uint32, _U, _P, _U, _P, C.c_int32, _P],
     "ntfg_tucker_factor_contract": [_V, C.c_int32, C.c_uint32, _U, _P, _U, _P, _P, C.c_uint32, _P],
     "ntfg_tucker_objective": [_V, C.c_int32, C.c_double, C.c_uint32, _U, _P, _U, _P, _P, _P],
+    "ntfg_tucker_jcomm_reference": [_V, C.c_int32, C.c_double, C.c_double, C.c_uint32, _U, _P, _U, _P, _P,
+                                    _P, _P],
+    "ntfg_tucker_jcomm_inner_update": [_V, C.c_int32, C.c_double, C.c_double, C.c_uint32, _U, _P, _P, _U, _P,
+                                       _P, _P, _P, C.c_int32],
     "ntfg_tucker_step": [_V, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, C.c_uint32, _U,
                          _P, _U, _P, _P, _P, _P, C.c_uint32],
 }

@@ -145,8 +145,10 @@ class JcommCpReference:
 
 @dataclass
 class JcommTuckerReference:
+    """reference tucker.hpp:59-63: the reference model and its P~/Q~."""
     ref: Tuple[np.ndarray, List[np.ndarray]]
-    x: np.ndarray
+    p: np.ndarray
+    q: np.ndarray
 
 
 def _prec(p) -> int:
@@ -375,7 +377,7 @@ def jcomm_fit(x, init, cfg: FitConfig, ctx: Optional[Context] = None, shard=None
     return _cp_fit(1, x, init, cfg, ctx, shard)
 
 
-def _cp_fit_coo(algo: int, indices, values, dims, init, cfg: FitConfig, ctx=None) -> CpFitResult:
+def _cp_fit_coo(algo: int, indices, values, dims, init, cfg: FitConfig, ctx=None, shard=None) -> CpFitResult:
     ctx = ctx or default_context()
     dims = [int(d) for d in dims]
     init = [_f64(a) for a in init]
@@ -408,20 +410,26 @@ def _cp_fit_coo(algo: int, indices, values, dims, init, cfg: FitConfig, ctx=None
     f = _cat(init)
     rows = (N.TraceRowC * (int(cfg.max_iters) + 1))()
     n = C.c_uint64(0)
+    sh = None if shard is None else N.ShardC(int(shard[0]), int(shard[1]))
     _check(N.load().ntfg_cp_fit_coo(ctx.h, C.byref(cfgc), algo, len(dims), _u64(dims).ctypes.data_as(_UP),
-                                    int(nnz), ip, vp, vdt, loc, _dp(f), rows, C.byref(n)))
+                                    int(nnz), ip, vp, vdt, loc, C.byref(sh) if sh is not None else None, _dp(f),
+                                    rows, C.byref(n)))
     return CpFitResult(_split(f, [a.shape for a in init]), _trace(rows, n.value))
 
 
-def bcomm_fit_coo(indices, values, dims, init, cfg: FitConfig, ctx: Optional[Context] = None) -> CpFitResult:
+def bcomm_fit_coo(indices, values, dims, init, cfg: FitConfig, ctx: Optional[Context] = None,
+                  shard=None) -> CpFitResult:
     """Block-MM CP fit of a sparse COO count tensor at beta = 1 (new; the
-    reference densifies COO input, io.cpp:87-142, then runs bcomm_fit)."""
-    return _cp_fit_coo(0, indices, values, dims, init, cfg, ctx)
+    reference densifies COO input, io.cpp:87-142, then runs bcomm_fit).
+    shard = (global_dim0, slab_begin): this rank's nonzeros, i_0 rebased to
+    its mode-0 slab (see dist.shard_coo)."""
+    return _cp_fit_coo(0, indices, values, dims, init, cfg, ctx, shard)
 
 
-def jcomm_fit_coo(indices, values, dims, init, cfg: FitConfig, ctx: Optional[Context] = None) -> CpFitResult:
+def jcomm_fit_coo(indices, values, dims, init, cfg: FitConfig, ctx: Optional[Context] = None,
+                  shard=None) -> CpFitResult:
     """Joint-MM CP fit of a sparse COO count tensor at beta = 1 (see bcomm_fit_coo)."""
-    return _cp_fit_coo(1, indices, values, dims, init, cfg, ctx)
+    return _cp_fit_coo(1, indices, values, dims, init, cfg, ctx, shard)
 
 
 def mu_unfold_cp_fit(x, init, cfg: FitConfig, ctx: Optional[Context] = None) -> CpFitResult:
@@ -798,20 +806,123 @@ def jcomm_tucker_outer_step(m, x, beta, inner_steps, eps, precision="f64", ctx=N
     return _tucker_step(3, m, x, beta, eps, inner=inner_steps, precision=precision, ctx=ctx)
 
 
-def make_jcomm_tucker_reference(ref, x, beta, eps) -> JcommTuckerReference:
-    """tucker.cpp:92-98 -- the cache is rebuilt on the device by the inner-update calls."""
-    core, fs = _check_tucker(ref[0], ref[1], list(np.shape(x)), "make_jcomm_tucker_reference")
-    return JcommTuckerReference((core.copy(), [a.copy() for a in fs]), _f64(x))
+def make_jcomm_tucker_reference(ref, x, beta, eps, precision="f64", ctx=None) -> JcommTuckerReference:
+    """tucker.cpp:92-98: P~/Q~ of the reference model, computed on the device."""
+    ctx = ctx or default_context()
+    x = _f64(x)
+    core, fs = _check_tucker(ref[0], ref[1], list(x.shape), "make_jcomm_tucker_reference")
+    p = np.zeros(x.shape)
+    q = np.zeros(x.shape)
+    _check(N.load().ntfg_tucker_jcomm_reference(ctx.h, _prec(precision), float(beta), float(eps), x.ndim,
+                                                _u64(x.shape).ctypes.data_as(_UP), _dp(x),
+                                                _u64(core.shape).ctypes.data_as(_UP), _dp(core), _dp(_cat(fs)),
+                                                _dp(p), _dp(q)))
+    return JcommTuckerReference((core.copy(), [a.copy() for a in fs]), p, q)
+
+
+def _tucker_inner(cur, ctx_ref: JcommTuckerReference, block, beta, eps, precision, ctx):
+    ctx = ctx or default_context()
+    p, q = _f64(ctx_ref.p), _f64(ctx_ref.q)
+    if p.shape != q.shape:
+        raise ShapeError("jcomm_inner_update: P/Q shape mismatch")
+    core, fs = _check_tucker(cur[0], cur[1], list(p.shape), "jcomm_inner_update")
+    rcore, rfs = _check_tucker(ctx_ref.ref[0], ctx_ref.ref[1], list(p.shape), "jcomm_inner_update")
+    c = core.copy()
+    f = _cat(fs)
+    _check(N.load().ntfg_tucker_jcomm_inner_update(ctx.h, _prec(precision), float(beta), float(eps), p.ndim,
+                                                   _u64(p.shape).ctypes.data_as(_UP), _dp(p), _dp(q),
+                                                   _u64(core.shape).ctypes.data_as(_UP), _dp(rcore),
+                                                   _dp(_cat(rfs)), _dp(c), _dp(f), int(block)))
+    return c, _split(f, [a.shape for a in fs])
 
 
 def jcomm_inner_core_update(cur, ctx_ref: JcommTuckerReference, beta, eps, precision="f64", ctx=None):
-    """tucker.cpp:100-114."""
-    return _tucker_step(4, cur, ctx_ref.x, beta, eps, ref=ctx_ref.ref, precision=precision, ctx=ctx)
+    """tucker.cpp:100-114 (from the cached host P~/Q~)."""
+    return _tucker_inner(cur, ctx_ref, -1, beta, eps, precision, ctx)
 
 
 def jcomm_inner_factor_update(cur, ctx_ref: JcommTuckerReference, mode, beta, eps, precision="f64",
                               ctx=None):
-    """tucker.cpp:116-136."""
+    """tucker.cpp:116-136 (from the cached host P~/Q~)."""
     if mode >= len(cur[1]):
         raise ShapeError("jcomm_inner_factor_update: mode out of range")
-    return _tucker_step(5, cur, ctx_ref.x, beta, eps, mode=mode, ref=ctx_ref.ref, precision=precision, ctx=ctx)
+    return _tucker_inner(cur, ctx_ref, int(mode), beta, eps, precision, ctx)
+
+
+# ---------------------------------------------------------------------------
+# BMMe step-level API (reference cp.hpp:80-110, tucker.hpp:88-106): factor-sized
+# host arithmetic as in the reference; the fit drivers run it on the device.
+
+@dataclass
+class ExtrapolationState:
+    previous: list
+    t: float = 1.0
+    alpha: float = 0.0
+    cap: float = 1.0
+    delta: float = 1e-6
+    eps: float = 1e-12
+    enabled: bool = False
+
+
+def _pos_sq(cur, prev) -> float:
+    cur, prev = np.asarray(cur, dtype=np.float64), np.asarray(prev, dtype=np.float64)
+    if cur.shape != prev.shape:
+        raise ShapeError("extrapolation: shape mismatch with recorded iterate")
+    d = cur - prev
+    d = d[d > 0.0]
+    return float(np.sum(d * d))
+
+
+def _blocks(model):
+    """CP: list of factors; Tucker: (core, factors) -> [core] + factors."""
+    if isinstance(model, tuple):
+        return [model[0]] + list(model[1])
+    return list(model)
+
+
+def make_extrapolation_state(initial, enabled: bool, cap: float, delta: float, eps: float) -> ExtrapolationState:
+    """CP factors or a Tucker (core, factors) model (make_tucker_extrapolation_state)."""
+    prev = (np.array(initial[0], copy=True), [np.array(a, copy=True) for a in initial[1]]) \
+        if isinstance(initial, tuple) else [np.array(a, copy=True) for a in initial]
+    return ExtrapolationState(prev, cap=float(cap), delta=float(delta), eps=float(eps), enabled=bool(enabled))
+
+
+make_tucker_extrapolation_state = make_extrapolation_state
+
+
+def extrapolation_begin_iteration(st: ExtrapolationState, current) -> None:
+    tn = 0.5 * (1.0 + np.sqrt(1.0 + 4.0 * st.t * st.t))
+    an = (st.t - 1.0) / tn
+    st.t = tn
+    cur, prev = _blocks(current), _blocks(st.previous)
+    if len(cur) != len(prev):
+        raise ShapeError("extrapolation: order mismatch")
+    sq = 0.0
+    for a, b in zip(cur, prev):
+        sq += _pos_sq(a, b)
+    st.alpha = min(an, st.cap / (np.sqrt(sq) + st.delta))
+
+
+def _inertial(cur, prev, alpha, eps):
+    cur, prev = np.asarray(cur, dtype=np.float64), np.asarray(prev, dtype=np.float64)
+    if cur.shape != prev.shape:
+        raise ShapeError("extrapolate_block: shape mismatch with recorded iterate")
+    d = cur - prev
+    return np.maximum(cur + alpha * np.where(d > 0.0, d, 0.0), eps)
+
+
+def extrapolate_block(current, st: ExtrapolationState, block: int) -> np.ndarray:
+    """CP: factor `block`; Tucker state: factor `block` (the core is extrapolate_core)."""
+    facs = st.previous[1] if isinstance(st.previous, tuple) else st.previous
+    if block >= len(facs):
+        raise ShapeError("extrapolate_block: block out of range")
+    return _inertial(current, facs[block], st.alpha, st.eps)
+
+
+def extrapolate_core(current, st: ExtrapolationState) -> np.ndarray:
+    return _inertial(current, st.previous[0], st.alpha, st.eps)
+
+
+def extrapolation_end_iteration(st: ExtrapolationState, iterate) -> None:
+    st.previous = (np.array(iterate[0], copy=True), [np.array(a, copy=True) for a in iterate[1]]) \
+        if isinstance(iterate, tuple) else [np.array(a, copy=True) for a in iterate]

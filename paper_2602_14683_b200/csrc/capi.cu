@@ -12,7 +12,7 @@ namespace ntfg {
 void cp_fit(Context&, const ntfg_fit_config&, int, uint32_t, const uint64_t*, const void*, int, int,
             const ntfg_shard*, double*, ntfg_trace_row*, uint64_t*);
 void cp_fit_coo(Context&, const ntfg_fit_config&, int, uint32_t, const uint64_t*, uint64_t, const int32_t*,
-                const void*, int, int, double*, ntfg_trace_row*, uint64_t*);
+                const void*, int, int, const ntfg_shard*, double*, ntfg_trace_row*, uint64_t*);
 void cp_reconstruct(Context&, int, uint32_t, const uint64_t*, uint64_t, const double*, double*);
 // unfold_api.cu
 void cp_mu_unfold_fit(Context&, const ntfg_fit_config&, uint32_t, const uint64_t*, const void*, int, int, double*,
@@ -58,6 +58,11 @@ void tucker_factor_contract(Context&, int, uint32_t, const uint64_t*, const doub
                             const uint64_t*, const double*, const double*, uint32_t, double*);
 void tucker_objective(Context&, int, double, uint32_t, const uint64_t*, const double*,
                       const uint64_t*, const double*, const double*, double*);
+void tucker_jcomm_reference(Context&, int, double, double, uint32_t, const uint64_t*, const double*,
+                            const uint64_t*, const double*, const double*, double*, double*);
+void tucker_jcomm_inner_update(Context&, int, double, double, uint32_t, const uint64_t*, const double*,
+                               const double*, const uint64_t*, const double*, const double*, double*, double*,
+                               int32_t);
 void tucker_step(Context&, int, int, double, double, uint64_t, uint32_t, const uint64_t*,
                  const double*, const uint64_t*, const double*, const double*, double*, double*,
                  uint32_t);
@@ -226,14 +231,14 @@ NTFG_API ntfg_status ntfg_cp_fit(ntfg_context* ctx, const ntfg_fit_config* cfg, 
 NTFG_API ntfg_status ntfg_cp_fit_coo(ntfg_context* ctx, const ntfg_fit_config* cfg, int32_t algo,
                                      uint32_t order, const uint64_t* dims, uint64_t nnz,
                                      const int32_t* indices, const void* values, int32_t values_dtype,
-                                     int32_t location, double* factors, ntfg_trace_row* trace,
-                                     uint64_t* trace_len) {
+                                     int32_t location, const ntfg_shard* shard, double* factors,
+                                     ntfg_trace_row* trace, uint64_t* trace_len) {
   return with_ctx(ctx, [&](ntfg::Context& c) {
     need(cfg, "cfg"); need(dims, "dims"); need(factors, "factors");
     need(trace, "trace"); need(trace_len, "trace_len");
     if (nnz > 0) { need(indices, "indices"); need(values, "values"); }
-    ntfg::cp_fit_coo(c, *cfg, algo, order, dims, nnz, indices, values, values_dtype, location, factors, trace,
-                     trace_len);
+    ntfg::cp_fit_coo(c, *cfg, algo, order, dims, nnz, indices, values, values_dtype, location, shard, factors,
+                     trace, trace_len);
   });
 }
 
@@ -497,5 +502,29 @@ NTFG_API ntfg_status ntfg_tucker_step(ntfg_context* ctx, int32_t precision, int3
     need(dims, "dims"); need(x, "x"); need(ranks, "ranks"); need(core, "core"); need(factors, "factors");
     ntfg::tucker_step(c, precision, kind, beta, eps, inner_steps, order, dims, x, ranks, ref_core,
                       ref_factors, core, factors, mode);
+  });
+}
+
+NTFG_API ntfg_status ntfg_tucker_jcomm_reference(ntfg_context* ctx, int32_t precision, double beta, double eps,
+                                                 uint32_t order, const uint64_t* dims, const double* x,
+                                                 const uint64_t* ranks, const double* ref_core,
+                                                 const double* ref_factors, double* p_out, double* q_out) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(x, "x"); need(ranks, "ranks"); need(ref_core, "ref_core");
+    need(ref_factors, "ref_factors"); need(p_out, "p_out"); need(q_out, "q_out");
+    ntfg::tucker_jcomm_reference(c, precision, beta, eps, order, dims, x, ranks, ref_core, ref_factors, p_out, q_out);
+  });
+}
+
+NTFG_API ntfg_status ntfg_tucker_jcomm_inner_update(ntfg_context* ctx, int32_t precision, double beta, double eps,
+                                                    uint32_t order, const uint64_t* dims, const double* p,
+                                                    const double* q, const uint64_t* ranks, const double* ref_core,
+                                                    const double* ref_factors, double* core, double* factors,
+                                                    int32_t block) {
+  return with_ctx(ctx, [&](ntfg::Context& c) {
+    need(dims, "dims"); need(p, "p"); need(q, "q"); need(ranks, "ranks"); need(ref_core, "ref_core");
+    need(ref_factors, "ref_factors"); need(core, "core"); need(factors, "factors");
+    ntfg::tucker_jcomm_inner_update(c, precision, beta, eps, order, dims, p, q, ranks, ref_core, ref_factors, core,
+                                    factors, block);
   });
 }

@@ -131,14 +131,14 @@ void cp_fit(Context& c, const ntfg_fit_config& cfg, int algo, uint32_t order, co
 // whatever cfg.precision says (the nonzero pass is latency-bound, not
 // bandwidth-bound, so fp32 storage buys nothing).
 void cp_fit_coo(Context& c, const ntfg_fit_config& cfg, int algo, uint32_t order, const uint64_t* dims,
-                uint64_t nnz, const int32_t* indices, const void* values, int dtype, int loc, double* factors,
-                ntfg_trace_row* trace, uint64_t* trace_len) {
+                uint64_t nnz, const int32_t* indices, const void* values, int dtype, int loc, const ntfg_shard* shard,
+                double* factors, ntfg_trace_row* trace, uint64_t* trace_len) {
   validate_config(cfg);
   if (algo != NTFG_BCOMM && algo != NTFG_JCOMM) throw Error(NTFG_ERR_DOMAIN, "unknown algorithm");
   c.stats = ntfg_stats{};
   std::vector<ntfg_trace_row> tr = cp_fit_t<double>(
       c, cfg, algo, order, dims,
-      [&](CpEngine<double>& e) { e.set_coo(nnz, indices, values, dtype, loc); }, nullptr, factors);
+      [&](CpEngine<double>& e) { e.set_coo(nnz, indices, values, dtype, loc); }, shard, factors);
   for (size_t i = 0; i < tr.size(); ++i) trace[i] = tr[i];
   *trace_len = tr.size();
 }

@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "coo_ingest.cuh"
 #include "coo_kernels.cuh"
 #include "cp_kernels.cuh"
 #include "engine.cuh"
@@ -311,8 +312,6 @@ class CpEngine {
     if (sizeof(T) != 4 || !tc_allowed_) return false;
     if (const char* e = std::getenv("NTFG_DISABLE_TC")) if (e[0] == '1') return false;
     if (g_.K % 128 != 0 || g_.K > 512 || R_ > 64 || g_.rows >= (int64_t(1) << 31)) return false;
-    const int N = tc_n();
-    if (2 * (g_.K / 128) * N > 256) return false;
     for (int n = 0; n < N_ - 1; ++n) {
       int64_t Bn = 1;
       for (int m = n + 1; m < N_ - 1; ++m) Bn *= g_.dims[m];
@@ -324,9 +323,17 @@ class CpEngine {
   // shared-memory plan of one contraction launch: A stages (1024-aligned),
   // B tiles, then the B producers' cp.async gather ring.  Deeper gathers first
   // (they hide the L2 latency of the factor rows), then more stages.
+  // m-tiles per work item: the epilogue keeps ns * mtw * N fp32 segment sums
+  // per thread in registers (<= 128)
+  int tc_mtw(int ns) const {
+    const int mt = int(g_.K / 128), N = tc_n();
+    int w = mt;
+    while (w > 1 && (ns * w * N > 128 || mt % w != 0)) --w;
+    return w;
+  }
   TcLayout tc_layout(int ns, int N, int nmm) const {
     TcLayout L{};
-    L.a_stream = uint32_t(2 * (g_.K / 64) * 2048);
+    L.a_stream = uint32_t(2 * (2 * tc_mtw(ns)) * 2048);
     L.a_stage = uint32_t(ns) * L.a_stream;
     L.b_tile = uint32_t(N / 8 * kTcBSbo);
     L.gmodes = std::max(1, std::min(nmm, kTcGModes));
@@ -366,6 +373,11 @@ class CpEngine {
 
   // work split of one tensor-core contraction: case A (last mode) = row
   // chunks, case B = (target index, split) pairs; chunk = rows per unit
+  // stages (of 16 rows) per TMEM accumulation segment (tc_contract.cuh, MMA issuers)
+  static int tc_seg_stages() {
+    static const int v = [] { const char* e = std::getenv("NTFG_TC_SEG"); return e ? std::max(1, std::atoi(e)) : 16; }();
+    return v;
+  }
   static int64_t tc_unit_rows_cap() {  // experiments: NTFG_TC_UNIT_ROWS caps the TMEM accumulation length
     static const int64_t v = [] { const char* e = std::getenv("NTFG_TC_UNIT_ROWS"); return e ? std::atoll(e) : 0; }();
     return v;
@@ -402,6 +414,9 @@ class CpEngine {
     p.N = tc_n();
     p.ns = ns;
     p.mt = int(g_.K / 128);
+    p.mtw = tc_mtw(ns);
+    p.G = p.mt / p.mtw;
+    p.seg = tc_seg_stages();
     p.caseA = caseA;
     const int64_t In = g_.dims[n];
     TcMaps maps{};
@@ -445,7 +460,7 @@ class CpEngine {
       p.lastfac[s] = p.fac32[s][N_ - 1];
       for (int h = 0; h < 2; ++h)
         if (!tc::make_plane_map(&maps.m[s][h], planes_[2 * st[s].plane + h], g_.K, mapB, mapI, mapA, p.boxB,
-                                p.boxA))
+                                p.boxA, 2 * p.mtw))
           throw Error(NTFG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     }
     stage_f32_kernel<<<int(std::min<int64_t>(ceil_div(fs.off[N_] * ns, 256), 1024)), 256, 0, c_.stream>>>(fs);
@@ -463,16 +478,16 @@ class CpEngine {
     }
     p.partA = reinterpret_cast<float*>(partA_);
     p.partB = partB_;
-    const int cols = ns * p.mt * p.N;
-    p.dbuf = 2 * cols <= 512 ? 1 : 0;
+    const int cols = ns * p.mtw * p.N;  // one segment buffer; two alternate, plus the running sums
     int alloc = 32;
-    while (alloc < (p.dbuf ? 2 : 1) * cols) alloc *= 2;
+    while (alloc < 3 * cols) alloc *= 2;
     p.tmem_cols = alloc;
+    p.items = p.units * p.G;
     {  // perf experiments only (tools/): role ablation bits, results are wrong when set
       static const int dbg = [] { const char* e = std::getenv("NTFG_TC_ABLATE"); return e ? std::atoi(e) : 0; }();
       p.ablate = dbg;
     }
-    const int grid = int(std::min<int64_t>(p.units, int64_t(c_.sm_count)));
+    const int grid = int(std::min<int64_t>(p.items, int64_t(c_.sm_count)));
     static const char* trace_path = std::getenv("NTFG_TC_TRACE");  // perf experiments (eager fits only)
     if (trace_path) {
       p.trace = reinterpret_cast<unsigned long long*>(c_.bufs.get("cp.tctrace", size_t(grid) * 17 * 8 * 8));
@@ -497,7 +512,7 @@ class CpEngine {
       }
     }
     units_out = p.units;
-    S_out = p.S;
+    S_out = caseA ? p.S : p.S * p.G;  // case B partials: [ns][In][S * G][RP]
   }
 
   struct Plan {
@@ -559,7 +574,7 @@ class CpEngine {
         int64_t units, S, chunk;
         tc_units(n, units, S, chunk);
         if (n == N_ - 1) a = std::max(a, size_t(ns) * units * g_.K * RP_);
-        else b = std::max(b, size_t(ns) * units * RP_);
+        else b = std::max(b, size_t(ns) * units * (g_.K / 128) * RP_);  // x G m-tile groups
       }
     partA_ = c_.buf<T>("cp.partA", std::max<size_t>(a, 1));
     partB_ = c_.buf<double>("cp.partB", std::max<size_t>(b, 1));
@@ -690,6 +705,7 @@ class CpEngine {
     if (sparse_) {
       if (objective && n != 0) coo_objective(fac);
       coo_num(n, fac, numden_, objective && n == 0);
+      if (sharded_ && n != 0) allreduce(numden_, size_t(g_.dims[n]) * R_);
       if (objective && n == 0) coo_finish_objective(fac);
       colprod(fac, n);
       coo_finalize(n, numden_, anchor, nullptr);
@@ -772,6 +788,7 @@ class CpEngine {
       for (int m = 0; m < N_; ++m) fac[m] = Aref_ + off_[m];
       for (int n = 0; n < N_; ++n) {
         coo_num(n, fac, n1num_ + off_[n], n == 0 && coo_pending_obj_);
+        if (sharded_ && n != 0) allreduce(n1num_ + off_[n], size_t(g_.dims[n]) * R_);
         if (n == 0 && coo_pending_obj_) coo_finish_objective(fac);
       }
       coo_pending_obj_ = false;
@@ -848,103 +865,168 @@ class CpEngine {
   }
 
   // ---- sparse COO data (K7, coo_kernels.cuh; beta = 1 only) -------------------------------
-  // indices: [nnz][order] int32 row-major (host or device), values fp32/fp64.
+  // indices: [nnz][order] int32 row-major (host or device), values fp32/fp64;
+  // in a data-parallel fit (shard) they are this rank's nonzeros with i_0
+  // local to its mode-0 slab (dims[0] = slab rows), exactly like a dense slab.
   // Duplicates are summed in input order (as read_coo's dense +=, io.cpp:138);
-  // one copy of the merged nonzeros per mode, stably sorted by that mode's index.
+  // one copy of the merged nonzeros per mode, stably sorted by that mode's
+  // index (coo_ingest.cuh: keys, radix sorts and scans on the device).
+  template <typename F>
+  void cub_call(const char* what, F&& f) {
+    size_t bytes = 0;
+    NTFG_CUDA(f(nullptr, bytes));
+    void* tmp = c_.bufs.get("coo.cubtmp", std::max<size_t>(bytes, 16));
+    cuda_check(f(tmp, bytes), what);
+  }
   void set_coo(uint64_t nnz, const int32_t* indices, const void* values, int dtype, int location) {
     if (beta_ != 1.0) throw Error(NTFG_ERR_DOMAIN, "sparse COO fits require beta = 1");
     if (R_ > 64) throw Error(NTFG_ERR_SHAPE, "sparse COO fits support rank <= 64");
-    if (sharded_) throw Error(NTFG_ERR_SHAPE, "sparse COO fits are single-device");
-    const size_t N = size_t(N_);
-    std::vector<int32_t> hidx(size_t(nnz) * N);
-    std::vector<double> hval(nnz);
-    if (location == NTFG_DEVICE) {
-      c_.d2h(hidx.data(), indices, hidx.size() * sizeof(int32_t));
-      if (dtype == 1) {
-        std::vector<float> f(nnz);
-        c_.d2h(f.data(), values, nnz * sizeof(float));
-        c_.sync();
-        for (size_t j = 0; j < nnz; ++j) hval[j] = f[j];
-      } else {
-        c_.d2h(hval.data(), values, nnz * sizeof(double));
-      }
-      c_.sync();
-    } else {
-      std::copy(indices, indices + hidx.size(), hidx.begin());
-      for (size_t j = 0; j < nnz; ++j)
-        hval[j] = dtype == 1 ? double(static_cast<const float*>(values)[j]) : static_cast<const double*>(values)[j];
+    if (nnz >= (uint64_t(1) << 31)) throw Error(NTFG_ERR_SHAPE, "sparse COO fits support < 2^31 nonzeros");
+    const int N = N_;
+    const int64_t n = int64_t(nnz);
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), int64_t(c_.sm_count) * 8)));
+    const size_t vbytes = dtype == 1 ? 4 : 8;
+    const int32_t* didx = indices;
+    const void* dval = values;
+    if (location != NTFG_DEVICE) {
+      int32_t* ti = c_.buf<int32_t>("coo.in_idx", std::max<size_t>(size_t(n) * N, 1));
+      void* tv = c_.bufs.get("coo.in_val", std::max<size_t>(size_t(n) * vbytes, 8));
+      c_.h2d(ti, indices, size_t(n) * N * sizeof(int32_t));
+      c_.h2d(tv, values, size_t(n) * vbytes);
+      didx = ti;
+      dval = tv;
     }
-    // linear keys (row-major) + stable order -> merged, lexicographically sorted nonzeros
-    std::vector<int64_t> key(nnz);
-    for (size_t j = 0; j < nnz; ++j) {
-      int64_t k = 0;
-      for (size_t m = 0; m < N; ++m) {
-        const int32_t i = hidx[j * N + m];
-        if (i < 0 || int64_t(i) >= g_.dims[m]) throw Error(NTFG_ERR_SHAPE, "COO index out of range");
-        k = k * g_.dims[m] + i;
-      }
-      key[j] = k;
+    // 1. linear keys + stable sort -> merged nonzeros (lexicographic order)
+    int64_t* key = c_.buf<int64_t>("coo.key", std::max<int64_t>(n, 1));
+    int64_t* key2 = c_.buf<int64_t>("coo.key2", std::max<int64_t>(n, 1));
+    int64_t* pos = c_.buf<int64_t>("coo.pos", std::max<int64_t>(n, 1));
+    int64_t* pos2 = c_.buf<int64_t>("coo.pos2", std::max<int64_t>(n, 1));
+    unsigned* bad = c_.buf<unsigned>("coo.bad", 1);
+    NTFG_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), c_.stream));
+    CooKeyParams kp{};
+    kp.order = N;
+    for (int m = 0; m < N; ++m) kp.dims[m] = g_.dims[m];
+    kp.nnz = n;
+    kp.idx = didx;
+    kp.key = key;
+    kp.pos = pos;
+    kp.bad = bad;
+    coo_key_kernel<<<grid, 256, 0, c_.stream>>>(kp);
+    NTFG_LAUNCHED(c_);
+    unsigned hbad = 0;
+    c_.d2h(&hbad, bad, sizeof(unsigned));
+    c_.sync();
+    if (hbad) throw Error(NTFG_ERR_SHAPE, "COO index out of range");
+    const int kbits = bits_for(std::max<int64_t>(E_, 2) - 1);
+    if (n > 0)
+      cub_call("cub SortPairs (keys)", [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(t, b, key, key2, pos, pos2, int(n), 0, kbits, c_.stream);
+      });
+    int32_t* head = c_.buf<int32_t>("coo.head", std::max<int64_t>(n, 1));
+    int32_t* uid = c_.buf<int32_t>("coo.uid", std::max<int64_t>(n, 1) + 1);
+    if (n > 0) {
+      coo_head_kernel<<<grid, 256, 0, c_.stream>>>(key2, n, head);
+      NTFG_LAUNCHED(c_);
+      cub_call("cub ExclusiveSum (heads)", [&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, head, uid, int(n), c_.stream);
+      });
     }
-    std::vector<int64_t> ord(nnz);
-    for (size_t j = 0; j < nnz; ++j) ord[j] = int64_t(j);
-    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
-    std::vector<int32_t> midx;
-    std::vector<double> mval;
-    midx.reserve(hidx.size());
-    mval.reserve(nnz);
-    for (size_t t = 0; t < nnz;) {
-      const int64_t k = key[ord[t]];
-      double v = 0.0;
-      const size_t first = size_t(ord[t]);
-      for (; t < nnz && key[ord[t]] == k; ++t) v += hval[ord[t]];
-      for (size_t m = 0; m < N; ++m) midx.push_back(hidx[first * N + m]);
-      mval.push_back(v);
-    }
-    const size_t M = mval.size();
-    coo_nnz_ = int64_t(M);
-    coo_.assign(N, CooMode{});
-    size_t max_pieces = 1;
-    for (int n = 0; n < N_; ++n) {
-      // stable counting sort by i_n
-      const int64_t In = g_.dims[n];
-      std::vector<int64_t> cnt(size_t(In) + 1, 0);
-      for (size_t j = 0; j < M; ++j) ++cnt[size_t(midx[j * N + n]) + 1];
-      for (int64_t i = 0; i < In; ++i) cnt[size_t(i) + 1] += cnt[size_t(i)];
-      std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1), perm(M);
-      for (size_t j = 0; j < M; ++j) perm[size_t(pos[size_t(midx[j * N + n])]++)] = int64_t(j);
-      // pieces of <= kCooPiece nonzeros inside one key
-      std::vector<int64_t> pstart, kpiece(size_t(In) + 1);
-      for (int64_t i = 0; i < In; ++i) {
-        kpiece[size_t(i)] = int64_t(pstart.size());
-        for (int64_t b = cnt[size_t(i)]; b < cnt[size_t(i) + 1]; b += kCooPiece) pstart.push_back(b);
-      }
-      kpiece[size_t(In)] = int64_t(pstart.size());
-      const int64_t np = int64_t(pstart.size());
-      pstart.push_back(int64_t(M));
-      CooMode& cm = coo_[size_t(n)];
-      cm.npieces = np;
-      max_pieces = std::max(max_pieces, size_t(np));
-      const std::string tag = "coo." + std::to_string(n) + ".";
-      std::vector<int32_t> col(M);
-      for (size_t m = 0; m < N; ++m) {
-        for (size_t j = 0; j < M; ++j) col[j] = midx[size_t(perm[j]) * N + m];
-        cm.idx[m] = c_.buf<int32_t>(tag + "idx" + std::to_string(m), std::max<size_t>(M, 1));
-        c_.h2d(cm.idx[m], col.data(), M * sizeof(int32_t));
-        c_.sync();
-      }
-      std::vector<double> v(M);
-      for (size_t j = 0; j < M; ++j) v[j] = mval[size_t(perm[j])];
-      cm.val = c_.buf<double>(tag + "val", std::max<size_t>(M, 1));
-      c_.h2d(cm.val, v.data(), M * sizeof(double));
-      cm.piece_start = c_.buf<int64_t>(tag + "pstart", pstart.size());
-      c_.h2d(cm.piece_start, pstart.data(), pstart.size() * sizeof(int64_t));
-      cm.key_piece = c_.buf<int64_t>(tag + "kpiece", kpiece.size());
-      c_.h2d(cm.key_piece, kpiece.data(), kpiece.size() * sizeof(int64_t));
+    int32_t last[2] = {0, 0};
+    if (n > 0) {
+      c_.d2h(&last[0], uid + (n - 1), sizeof(int32_t));
+      c_.d2h(&last[1], head + (n - 1), sizeof(int32_t));
       c_.sync();
     }
-    coo_partial_ = c_.buf<double>("coo.partial", max_pieces * size_t(R_));
-    coo_obj_ = c_.buf<double>("coo.obj", max_pieces);
+    const int64_t M = n > 0 ? int64_t(last[0]) + last[1] : 0;
+    coo_nnz_ = M;
+    int32_t* midx[kMaxOrder] = {};
+    for (int m = 0; m < N; ++m) midx[m] = c_.buf<int32_t>("coo.m.idx" + std::to_string(m), std::max<int64_t>(M, 1));
+    double* mval = c_.buf<double>("coo.m.val", std::max<int64_t>(M, 1));
+    if (n > 0) {
+      CooMergeParams mp{};
+      mp.order = N;
+      mp.n = n;
+      mp.key = key2;
+      mp.pos = pos2;
+      mp.head = head;
+      mp.uid = uid;
+      mp.idx = didx;
+      mp.val = dval;
+      mp.f32 = dtype == 1;
+      for (int m = 0; m < N; ++m) mp.midx[m] = midx[m];
+      mp.mval = mval;
+      coo_merge_kernel<<<grid, 256, 0, c_.stream>>>(mp);
+      NTFG_LAUNCHED(c_);
+    }
+    // 2. per mode: stable sort by i_n, gather, cut into pieces
+    const int mgrid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(M, 256), int64_t(c_.sm_count) * 8)));
+    int32_t* iota = c_.buf<int32_t>("coo.iota", std::max<int64_t>(M, 1));
+    int32_t* perm = c_.buf<int32_t>("coo.perm", std::max<int64_t>(M, 1));
+    int32_t* skeys = c_.buf<int32_t>("coo.skeys", std::max<int64_t>(M, 1));
+    coo_iota_kernel<<<mgrid, 256, 0, c_.stream>>>(M, iota);
+    NTFG_LAUNCHED(c_);
+    coo_.assign(size_t(N), CooMode{});
+    int64_t max_pieces = 1;
+    for (int md = 0; md < N; ++md) {
+      const int64_t In = g_.dims[md];
+      const std::string tag = "coo." + std::to_string(md) + ".";
+      CooMode& cm = coo_[size_t(md)];
+      if (M > 0)
+        cub_call("cub SortPairs (mode)", [&](void* t, size_t& b) {
+          return cub::DeviceRadixSort::SortPairs(t, b, midx[md], skeys, iota, perm, int(M), 0, bits_for(In),
+                                                 c_.stream);
+        });
+      CooGatherParams gp{};
+      gp.order = N;
+      gp.n = M;
+      gp.perm = perm;
+      for (int m = 0; m < N; ++m) {
+        gp.src_idx[m] = midx[m];
+        cm.idx[m] = c_.buf<int32_t>(tag + "idx" + std::to_string(m), std::max<int64_t>(M, 1));
+        gp.dst_idx[m] = cm.idx[m];
+      }
+      gp.src_val = mval;
+      cm.val = c_.buf<double>(tag + "val", std::max<int64_t>(M, 1));
+      gp.dst_val = cm.val;
+      if (M > 0) {
+        coo_gather_kernel<<<mgrid, 256, 0, c_.stream>>>(gp);
+        NTFG_LAUNCHED(c_);
+      }
+      int32_t* cnt = c_.buf<int32_t>("coo.cnt", size_t(In) + 1);
+      int64_t* cnt64 = c_.buf<int64_t>("coo.cnt64", size_t(In) + 1);
+      int64_t* start = c_.buf<int64_t>("coo.start", size_t(In) + 1);
+      int64_t* np = c_.buf<int64_t>("coo.np", size_t(In) + 1);
+      cm.key_piece = c_.buf<int64_t>(tag + "kpiece", size_t(In) + 1);
+      NTFG_CUDA(cudaMemsetAsync(cnt, 0, (size_t(In) + 1) * sizeof(int32_t), c_.stream));
+      NTFG_CUDA(cudaMemsetAsync(np, 0, (size_t(In) + 1) * sizeof(int64_t), c_.stream));
+      if (M > 0) {
+        coo_count_kernel<<<mgrid, 256, 0, c_.stream>>>(cm.idx[md], M, cnt);
+        NTFG_LAUNCHED(c_);
+      }
+      const int kgrid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(In + 1, 256), int64_t(c_.sm_count) * 8)));
+      widen_kernel<<<kgrid, 256, 0, c_.stream>>>(cnt, In + 1, cnt64);
+      NTFG_LAUNCHED(c_);
+      cub_call("cub ExclusiveSum (starts)", [&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, cnt64, start, int(In + 1), c_.stream);
+      });
+      coo_npieces_kernel<<<kgrid, 256, 0, c_.stream>>>(cnt, In, np);
+      NTFG_LAUNCHED(c_);
+      cub_call("cub ExclusiveSum (pieces)", [&](void* t, size_t& b) {
+        return cub::DeviceScan::ExclusiveSum(t, b, np, cm.key_piece, int(In + 1), c_.stream);
+      });
+      int64_t total = 0;
+      c_.d2h(&total, cm.key_piece + In, sizeof(int64_t));
+      c_.sync();
+      cm.npieces = total;
+      max_pieces = std::max(max_pieces, total);
+      cm.piece_start = c_.buf<int64_t>(tag + "pstart", size_t(total) + 1);
+      coo_pieces_kernel<<<kgrid, 256, 0, c_.stream>>>(start, cnt, cm.key_piece, In, M, cm.piece_start);
+      NTFG_LAUNCHED(c_);
+    }
+    coo_partial_ = c_.buf<double>("coo.partial", size_t(max_pieces) * size_t(R_));
+    coo_obj_ = c_.buf<double>("coo.obj", size_t(max_pieces));
     coo_closed_ = c_.buf<double>("coo.closed", 1);
+    c_.sync();
     sparse_ = true;
     tc_ = false;
   }
@@ -994,9 +1076,19 @@ class CpEngine {
   }
   // D_1 = [nnz part] + sum_r prod_m colsum(A_m)(r), mean over all entries
   void coo_finish_objective(const double* const* fac) {
-    colprod(fac, -1);
+    colprod(fac, -1);  // global column sums (the mode-0 part is allreduced when sharded)
     closed_sum_kernel<<<1, 32, 0, c_.stream>>>(colprod_, int(R_), coo_closed_);
     NTFG_LAUNCHED(c_);
+    if (sharded_) {  // nnz part: local sum -> allreduce; the closed-form part once
+      objective_finalize_kernel<<<1, 256, 0, c_.stream>>>(coo_obj_, int(coo_[0].npieces), 1.0, losses_, counter_,
+                                                         raw_);
+      NTFG_LAUNCHED(c_);
+      allreduce(raw_, 1);
+      objective_finalize_kernel<<<1, 32, 0, c_.stream>>>(raw_, 1, 1.0 / double(E_global_), losses_, counter_,
+                                                        nullptr, coo_closed_);
+      NTFG_LAUNCHED(c_);
+      return;
+    }
     objective_finalize_kernel<<<1, 256, 0, c_.stream>>>(coo_obj_, int(coo_[0].npieces), 1.0 / double(E_global_),
                                                        losses_, counter_, nullptr, coo_closed_);
     NTFG_LAUNCHED(c_);

@@ -481,23 +481,43 @@ TuckerModel tucker_bcomm_sweep(const TuckerModel& m, const DenseTensor& x, const
     return tucker_step(2, m, x, p, eps, 0, 1, nullptr, nullptr);
 }
 
-JcommTuckerReference make_jcomm_tucker_reference(const TuckerModel& ref, const DenseTensor& x, const BetaParam&,
-                                                 double) {
+JcommTuckerReference make_jcomm_tucker_reference(const TuckerModel& ref, const DenseTensor& x, const BetaParam& p,
+                                                 double eps) {
     require_dims(ref.factors, x, "make_jcomm_tucker_reference");
-    return {ref, x};
+    JcommTuckerReference out{ref, DenseTensor(x.shape()), DenseTensor(x.shape())};
+    const auto flat = concat(ref.factors);
+    const auto dims = u64(x.shape());
+    const auto ranks = u64(ref.core.shape());
+    ok(ntfg_tucker_jcomm_reference(ctx(), NTFG_F64, p.beta(), eps, std::uint32_t(dims.size()), dims.data(), x.data(),
+                                   ranks.data(), ref.core.data(), flat.data(), out.p.data(), out.q.data()));
+    return out;
+}
+
+static TuckerModel tucker_inner(const TuckerModel& current, const JcommTuckerReference& c, int block,
+                                const BetaParam& p, double eps) {
+    require_dims(current.factors, c.p, "jcomm_inner_update");
+    if (c.q.shape() != c.p.shape()) throw ShapeError("jcomm_inner_update: P/Q shape mismatch");
+    TuckerModel g = current;
+    auto flat = concat(g.factors);
+    const auto rf = concat(c.ref.factors);
+    const auto dims = u64(c.p.shape());
+    const auto ranks = u64(current.core.shape());
+    ok(ntfg_tucker_jcomm_inner_update(ctx(), NTFG_F64, p.beta(), eps, std::uint32_t(dims.size()), dims.data(),
+                                      c.p.data(), c.q.data(), ranks.data(), c.ref.core.data(), rf.data(),
+                                      g.core.data(), flat.data(), block));
+    split_into(flat, g.factors);
+    return g;
 }
 
 TuckerModel jcomm_inner_core_update(const TuckerModel& current, const JcommTuckerReference& c, const BetaParam& p,
                                     double eps) {
-    const auto rf = concat(c.ref.factors);
-    return tucker_step(4, current, c.x, p, eps, 0, 1, c.ref.core.data(), rf.data());
+    return tucker_inner(current, c, -1, p, eps);
 }
 
 TuckerModel jcomm_inner_factor_update(const TuckerModel& current, const JcommTuckerReference& c, std::size_t mode,
                                       const BetaParam& p, double eps) {
     if (mode >= current.order()) throw ShapeError("jcomm_inner_factor_update: mode out of range");
-    const auto rf = concat(c.ref.factors);
-    return tucker_step(5, current, c.x, p, eps, mode, 1, c.ref.core.data(), rf.data());
+    return tucker_inner(current, c, int(mode), p, eps);
 }
 
 TuckerModel jcomm_tucker_outer_step(const TuckerModel& m, const DenseTensor& x, const BetaParam& p,
@@ -796,5 +816,111 @@ TuckerFitResult mu_unfold_tucker_fit(const DenseTensor& x, TuckerModel init, con
     split_into(flat, out.model.factors);
     return out;
 }
+
+}  // namespace ntf
+
+// ---- BMMe step-level API (reference cp.hpp:80-110, tucker.hpp:88-106) -----------------
+namespace ntf {
+namespace {
+// sum over i of ([cur_i - prev_i]_+)^2
+double pos_sq(const std::vector<double>& cur, const std::vector<double>& prev) {
+    if (cur.size() != prev.size()) throw ShapeError("extrapolation: shape mismatch with recorded iterate");
+    double s = 0.0;
+    for (std::size_t i = 0; i < cur.size(); ++i) {
+        const double d = cur[i] - prev[i];
+        if (d > 0.0) s += d * d;
+    }
+    return s;
+}
+// max(cur + alpha [cur - prev]_+, eps)
+void inertial(const std::vector<double>& cur, const std::vector<double>& prev, double alpha, double eps,
+              std::vector<double>& out) {
+    out.resize(cur.size());
+    for (std::size_t i = 0; i < cur.size(); ++i) {
+        const double d = cur[i] - prev[i];
+        const double v = cur[i] + alpha * (d > 0.0 ? d : 0.0);
+        out[i] = v < eps ? eps : v;
+    }
+}
+// Nesterov: alpha_k = (t_k - 1) / t_{k+1}, t_{k+1} = (1 + sqrt(1 + 4 t_k^2)) / 2
+double nesterov_step(double& t) {
+    const double tn = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
+    const double a = (t - 1.0) / tn;
+    t = tn;
+    return a;
+}
+}  // namespace
+
+ExtrapolationState make_extrapolation_state(const CpFactors& initial, bool enabled, double cap, double delta,
+                                            double eps) {
+    ExtrapolationState st;
+    st.previous = initial;
+    st.enabled = enabled;
+    st.cap = cap;
+    st.delta = delta;
+    st.eps = eps;
+    return st;
+}
+
+void extrapolation_begin_iteration(ExtrapolationState& st, const CpFactors& current) {
+    if (current.order() != st.previous.order()) throw ShapeError("extrapolation: order mismatch");
+    const double an = nesterov_step(st.t);
+    double sq = 0.0;
+    for (std::size_t n = 0; n < current.order(); ++n)
+        sq += pos_sq(current.factors[n].values(), st.previous.factors[n].values());
+    st.alpha = std::min(an, st.cap / (std::sqrt(sq) + st.delta));
+}
+
+Matrix extrapolate_block(const Matrix& current, const ExtrapolationState& st, std::size_t block) {
+    if (block >= st.previous.order()) throw ShapeError("extrapolate_block: block out of range");
+    const Matrix& prev = st.previous.factors[block];
+    if (prev.rows() != current.rows() || prev.cols() != current.cols())
+        throw ShapeError("extrapolate_block: shape mismatch with recorded iterate");
+    Matrix out(current.rows(), current.cols());
+    inertial(current.values(), prev.values(), st.alpha, st.eps, out.values());
+    return out;
+}
+
+void extrapolation_end_iteration(ExtrapolationState& st, const CpFactors& iterate) { st.previous = iterate; }
+
+TuckerExtrapolationState make_tucker_extrapolation_state(const TuckerModel& initial, bool enabled, double cap,
+                                                         double delta, double eps) {
+    TuckerExtrapolationState st;
+    st.previous = initial;
+    st.enabled = enabled;
+    st.cap = cap;
+    st.delta = delta;
+    st.eps = eps;
+    return st;
+}
+
+void extrapolation_begin_iteration(TuckerExtrapolationState& st, const TuckerModel& current) {
+    if (current.order() != st.previous.order()) throw ShapeError("extrapolation: order mismatch");
+    const double an = nesterov_step(st.t);
+    double sq = pos_sq(current.core.values(), st.previous.core.values());
+    for (std::size_t n = 0; n < current.order(); ++n)
+        sq += pos_sq(current.factors[n].values(), st.previous.factors[n].values());
+    st.alpha = std::min(an, st.cap / (std::sqrt(sq) + st.delta));
+}
+
+DenseTensor extrapolate_core(const DenseTensor& current, const TuckerExtrapolationState& st) {
+    if (current.shape() != st.previous.core.shape())
+        throw ShapeError("extrapolate_core: shape mismatch with recorded iterate");
+    DenseTensor out(current.shape());
+    inertial(current.values(), st.previous.core.values(), st.alpha, st.eps, out.values());
+    return out;
+}
+
+Matrix extrapolate_block(const Matrix& current, const TuckerExtrapolationState& st, std::size_t mode) {
+    if (mode >= st.previous.order()) throw ShapeError("extrapolate_block: mode out of range");
+    const Matrix& prev = st.previous.factors[mode];
+    if (prev.rows() != current.rows() || prev.cols() != current.cols())
+        throw ShapeError("extrapolate_block: shape mismatch with recorded iterate");
+    Matrix out(current.rows(), current.cols());
+    inertial(current.values(), prev.values(), st.alpha, st.eps, out.values());
+    return out;
+}
+
+void extrapolation_end_iteration(TuckerExtrapolationState& st, const TuckerModel& iterate) { st.previous = iterate; }
 
 }  // namespace ntf

@@ -137,6 +137,26 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+// 32 lanes x 16 consecutive 32-bit columns (no wait: pair with tmem_ld_wait)
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
 // ---- host: 5-D tensor map over one bf16 plane viewed as (ki, ko, b, i, a) ----------
 // element (row, k) of the plane with row = a*(In*Bn) + i*Bn + b lives at
 // ((a*In + i)*Bn + b)*K + ko*64 + ki.  Box = (64, boxB, 1, boxA, K/64): all
@@ -144,7 +164,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 // tiles with the 128-byte swizzle (two canonical MN-major SW128 atoms along K
 // each).
 inline bool make_plane_map(CUtensorMap* map, const void* base, int64_t K, int64_t Bn, int64_t In, int64_t An,
-                           int boxB, int boxA) {
+                           int boxB, int boxA, int nblk) {
   using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -162,7 +182,8 @@ inline bool make_plane_map(CUtensorMap* map, const void* base, int64_t K, int64_
   // instead of K/64.
   const cuuint64_t dims[5] = {64, cuuint64_t(Bn), cuuint64_t(In), cuuint64_t(An), cuuint64_t(K / 64)};
   const cuuint64_t strides[4] = {cuuint64_t(K * 2), cuuint64_t(Bn * K * 2), cuuint64_t(In * Bn * K * 2), 128};
-  const cuuint32_t box[5] = {64, cuuint32_t(boxB), 1, cuuint32_t(boxA), cuuint32_t(K / 64)};
+  // nblk 64-column blocks per box (a work item's m-tile group: 2 * mtw)
+  const cuuint32_t box[5] = {64, cuuint32_t(boxB), 1, cuuint32_t(boxA), cuuint32_t(nblk)};
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

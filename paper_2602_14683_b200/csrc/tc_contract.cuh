@@ -49,7 +49,7 @@ template <int N> __host__ __device__ constexpr int tc_issuers() { return N <= 32
 template <int N> __host__ __device__ constexpr int tc_threads() { return 352 + 32 * (tc_issuers<N>() - 1); }
 constexpr int kTcBSbo = 272;    // bytes between 8-column groups of a B tile (256 + 16: bank spread)
 constexpr int kTcGModes = 3;    // factor modes gathered through the cp.async ring (more: direct fp64)
-constexpr size_t kTcSmemMax = 227 * 1024 - 2560;  // dynamic budget (static smem 2.3 KB)
+constexpr size_t kTcSmemMax = 227 * 1024 - 5120;  // dynamic budget (static smem 4.3 KB + 1 KB alignment slack)
 
 // runtime shared-memory layout (host-computed, tc_layout)
 struct TcLayout {
@@ -65,8 +65,11 @@ struct TcParams {
   Geom g;
   int n, R, RP, N;       // target mode, rank, partial stride, UMMA N (16/32/64)
   int ns, mt;            // streams, 128-column m-tiles (K / 128)
+  int mtw, G;            // m-tiles per work item, m-tile groups (mt = mtw * G)
+  int seg;               // stages per TMEM accumulation segment
   int caseA;
   int64_t units, S, An, Bn;
+  int64_t items;         // work items = units * G
   int64_t chunk;         // rows per unit (multiple of 16, case A) / j per split (case B)
   int boxB, boxA;        // TMA box for the 16 rows of a stage
   FastDiv fB;
@@ -78,7 +81,7 @@ struct TcParams {
   TcLayout lay;
   float* partA;          // [ns][units][K][RP]
   double* partB;         // [ns][In][S][RP]
-  int tmem_cols, dbuf;   // allocation, double-buffered accumulator?
+  int tmem_cols;         // allocation (two segment buffers of ns * mtw * N columns)
   int ablate;            // perf experiments (NTFG_TC_ABLATE): 1 no B work, 2 no MMAs, 4 no epilogue work
   unsigned long long* trace;  // perf experiments: [cta][16 unit iterations][8] clock64 events (nullable)
 };
@@ -108,7 +111,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   __shared__ uint64_t a_full[kTcMaxStages], b_full[kTcMaxStages], empty[kTcMaxStages], acc_full[2], acc_empty[2];
   __shared__ uint64_t g_full[kTcMaxGather], g_empty[kTcMaxGather];
   __shared__ uint32_t tmem_base;
-  __shared__ double red[4][64];
+  __shared__ double red[4][128];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t K = p.g.K;
@@ -141,7 +144,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const int cols_per_buf = p.ns * p.mt * N;
+  const int cols_per_buf = p.ns * p.mtw * N;  // one accumulation segment buffer (<= 128 columns)
 
   auto unit_range = [&](int64_t u, int64_t& j0, int64_t& j1, int64_t& itgt, int64_t& split) {
     if (p.caseA) {
@@ -173,9 +176,11 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     // ================= TMA producer =================
     if (lane == 0) {
       uint32_t q = 0;
-      const unsigned bytes = unsigned(p.ns) * 2u * unsigned(K / 64) * 2048u;
+      const unsigned bytes = unsigned(p.ns) * 2u * unsigned(2 * p.mtw) * 2048u;
       unsigned long long tw = 0, t00 = p.trace ? clock64() : 0;
-      for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+      for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
+        const int64_t u = w / p.G;
+        const int blk0 = int(w % p.G) * 2 * p.mtw;  // first 64-column block of this item's m-tiles
         int64_t j0, j1, itgt, split;
         unit_range(u, j0, j1, itgt, split);
         for (int64_t j = j0; j < j1; j += kTcRows, ++q) {
@@ -193,7 +198,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
           }
           for (int s = 0; s < p.ns; ++s)
             for (int plane = 0; plane < 2; ++plane)
-              tc::tma_load_5d(stage_a(slot, s, plane), &maps.m[s][plane], 0, c2, c3, c4, 0, &a_full[slot]);
+              tc::tma_load_5d(stage_a(slot, s, plane), &maps.m[s][plane], 0, c2, c3, c4, blk0, &a_full[slot]);
         }
       }
       if (p.trace) {
@@ -203,58 +208,55 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     }
   } else if (warp == 9 || (warp == 11 && tc_issuers<NMAX>() > 1)) {
     // ================= MMA issuers =================
-    // issuer i (warp 9: 0, warp 11: 1) owns the accumulator tiles (s, m) with
-    // (s * mt + m) % 2 == i; each commits every stage slot and unit buffer
-    // (barrier counts kTcIssuers)
+    // issuer i (warp 9: 0, warp 11: 1) owns the accumulator tiles t = s * mtw + m
+    // with t % 2 == i; each commits every stage slot and segment buffer
+    // (barrier counts kTcIssuers).  The accumulator restarts from zero every
+    // p.seg stages (a "segment", alternating between two TMEM buffers) and the
+    // epilogue adds the segment sums on the CUDA cores: long fp32 accumulation
+    // chains inside the tensor core drift low (measured: C2 beta = 1 factors
+    // 1.3e-3 off the fp64 build after 100 outer iterations with 111-stage
+    // chains, 3.5e-5 with 16-stage chains), the CUDA-core sums round to nearest.
     const int issuer = warp == 9 ? 0 : 1;
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_bf16_f32(128, N, true, false);
-      uint32_t q = 0, it = 0;
-      for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++it) {
+      const int ntile = p.ns * p.mtw;
+      uint32_t q = 0, sc = 0;
+      for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
         int64_t j0, j1, itgt, split;
-        unit_range(u, j0, j1, itgt, split);
-        const uint32_t tb = p.dbuf ? (it & 1u) : 0u;
-        const uint32_t use = p.dbuf ? (it >> 1) : it;  // uses of this accumulator buffer so far
-        unsigned long long* tr = (p.trace && it < 16 && issuer == 0) ? p.trace + (size_t(blockIdx.x) * 16 + it) * 8 : nullptr;
-        if (tr) tr[2] = clock64();
-        tc::wait(&acc_empty[tb], (use & 1u) ^ 1u);
-        tc::fence_after_sync();
-        if (tr) tr[3] = clock64();
-        unsigned long long wa = 0, wb = 0;
+        unit_range(w / p.G, j0, j1, itgt, split);
+        uint32_t tb = 0;
         bool first = true;
-        for (int64_t j = j0; j < j1; j += kTcRows, ++q) {
+        int qi = 0;
+        for (int64_t j = j0; j < j1; j += kTcRows, ++q, ++qi) {
+          if (qi == 0) {  // segment start: wait until the epilogue drained this buffer
+            tb = sc & 1u;
+            tc::wait(&acc_empty[tb], ((sc >> 1) & 1u) ^ 1u);
+            tc::fence_after_sync();
+            first = true;
+          }
           const int slot = int(q % unsigned(L.nst));
           const uint32_t ph = (q / unsigned(L.nst)) & 1u;
-          unsigned long long t0 = tr ? clock64() : 0;
           tc::wait(&a_full[slot], ph);
-          unsigned long long t1 = tr ? clock64() : 0;
           tc::wait(&b_full[slot], ph);
-          if (tr) {
-            wa += t1 - t0;
-            wb += clock64() - t1;
-          }
           tc::fence_after_sync();
-          for (int s = 0; s < p.ns && !(p.ablate & 2); ++s) {
+          for (int t = issuer; t < ntile && !(p.ablate & 2); t += tc_issuers<NMAX>()) {
+            const int s = t / p.mtw, m = t - s * p.mtw;
             const uint64_t bh = tc::desc_k_interleave(stage_b(slot, s, 0), 128, kTcBSbo);
             const uint64_t bl = tc::desc_k_interleave(stage_b(slot, s, 1), 128, kTcBSbo);
-            for (int m = 0; m < p.mt; ++m) {
-              if (((s * p.mt + m) % tc_issuers<NMAX>()) != issuer) continue;
-              const uint32_t d = tmem + tb * uint32_t(cols_per_buf) + uint32_t((s * p.mt + m) * N);
-              const uint64_t ah = tc::desc_mn_sw128(stage_a(slot, s, 0) + size_t(m) * 4096, 2048, 1024);
-              const uint64_t al = tc::desc_mn_sw128(stage_a(slot, s, 1) + size_t(m) * 4096, 2048, 1024);
-              tc::mma_bf16(d, ah, bh, idesc, !first);
-              tc::mma_bf16(d, ah, bl, idesc, true);
-              tc::mma_bf16(d, al, bh, idesc, true);
-            }
+            const uint32_t d = tmem + tb * uint32_t(cols_per_buf) + uint32_t(t * N);
+            const uint64_t ah = tc::desc_mn_sw128(stage_a(slot, s, 0) + size_t(m) * 4096, 2048, 1024);
+            const uint64_t al = tc::desc_mn_sw128(stage_a(slot, s, 1) + size_t(m) * 4096, 2048, 1024);
+            tc::mma_bf16(d, ah, bh, idesc, !first);
+            tc::mma_bf16(d, ah, bl, idesc, true);
+            tc::mma_bf16(d, al, bh, idesc, true);
           }
           tc::commit(&empty[slot]);
           first = false;
-        }
-        tc::commit(&acc_full[tb]);
-        if (tr) {
-          tr[4] = wa;
-          tr[5] = wb;
-          tr[7] = clock64();
+          if (qi == p.seg - 1 || j + kTcRows >= j1) {  // segment end
+            tc::commit(&acc_full[tb]);
+            ++sc;
+            qi = -1;
+          }
         }
       }
     }
@@ -282,9 +284,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     uint32_t q = 0;
     unsigned long long gw = 0, g00 = p.trace ? clock64() : 0;
     if (gm > 0 && !(p.ablate & 1)) {
-      for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+      for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
         int64_t j0, j1, itgt, split;
-        unit_range(u, j0, j1, itgt, split);
+        unit_range(w / p.G, j0, j1, itgt, split);
         for (int64_t jb = j0; jb < j1; jb += kTcRows, ++q) {
           const int gs = int(q % unsigned(L.gdepth));
           const unsigned long long tq = p.trace ? clock64() : 0;
@@ -337,9 +339,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     constexpr int kMaxItems = 2;  // ns * 2 * N <= 256
     uint32_t q = 0;
     unsigned long long bw0 = 0, bw1 = 0, b00 = p.trace ? clock64() : 0;
-    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+    for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
       int64_t j0, j1, itgt, split;
-      unit_range(u, j0, j1, itgt, split);
+      unit_range(w / p.G, j0, j1, itgt, split);
       for (int64_t jb = j0; jb < j1; jb += kTcRows, ++q) {
         const int slot = int(q % unsigned(L.nst));
         if (p.ablate & 1) {
@@ -421,98 +423,118 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     }
   } else {
     // ================= epilogue (warps 4..7: TMEM lane quarter = warp % 4) =================
+    // Per segment: this thread's k row (lane) of the segment buffer is added
+    // into a running-sum region of TMEM (columns 2 * cols_per_buf ..) with
+    // CUDA-core fp32 adds (round to nearest; tcgen05.ld -> FADD -> tcgen05.st).
+    // Per work item: case A writes the [K][RP] partial of its m-tile group;
+    // case B dots G with the last-mode factor over k: out(r) = sum_k
+    // F_last(k, r) G(k, r) (fp64 across k, m-tiles and units).
     const int quarter = warp & 3;
     const int et = tid - 128;  // 0..127
-    // case B: out(r) = sum_k F_last(k, r) G(k, r) over this thread's k = m*128 +
-    // 32*quarter + lane, in steps (stream s, column chunk c, m-tile m).  The
-    // F_last values of a step do not depend on the accumulator, so they are
-    // loaded one step ahead (16-byte loads of the padded [K][N] fp32 copy) and
-    // the L2 round trip overlaps the previous step's TMEM read + FMAs.
-    constexpr int CW = N < 32 ? N : 32;
-    constexpr int NC = N / CW;
-    constexpr int V4 = CW / 4;
-    const int nsteps = p.ns * NC * p.mt;
-    float4 cur[V4], nxt[V4];
-    auto load_lf = [&](int step, float4(&dst)[V4]) {
-      const int m = step % p.mt;
-      const int c = (step / p.mt) % NC;
-      const int s = step / (p.mt * NC);
-      const int64_t k = int64_t(m) * 128 + quarter * 32 + lane;
-      const float4* src = reinterpret_cast<const float4*>((s ? p.lastfac[1] : p.lastfac[0]) + k * N + c * CW);
-#pragma unroll
-      for (int j = 0; j < V4; ++j) dst[j] = __ldg(src + j);
-    };
-    if (!p.caseA) load_lf(0, cur);
-    uint32_t it = 0;
-    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++it) {
+    const int ntile = p.ns * p.mtw;
+    const int nchunk = ntile * N / 16;
+    const uint32_t lanes = uint32_t(quarter * 32) << 16;
+    const uint32_t run = tmem + lanes + 2u * uint32_t(cols_per_buf);
+    uint32_t sc = 0;
+    for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
+      const int64_t u = w / p.G;
+      const int g = int(w % p.G);
       int64_t j0, j1, itgt, split;
       unit_range(u, j0, j1, itgt, split);
-      const uint32_t tb = p.dbuf ? (it & 1u) : 0u;
-      const uint32_t use = p.dbuf ? (it >> 1) : it;
-      tc::wait(&acc_full[tb], use & 1u);
-      tc::fence_after_sync();
-      unsigned long long* tr = (p.trace && it < 16 && et == 0) ? p.trace + (size_t(blockIdx.x) * 16 + it) * 8 : nullptr;
-      if (tr) tr[0] = clock64();
-      const uint32_t tbase = tmem + (uint32_t(quarter * 32) << 16) + tb * uint32_t(cols_per_buf);
-      if (p.ablate & 4) {
-      } else if (p.caseA) {
-        for (int s = 0; s < p.ns; ++s) {
-          for (int m = 0; m < p.mt; ++m) {
-            const int64_t k = int64_t(m) * 128 + quarter * 32 + lane;
+      const int64_t nstage = (j1 - j0 + kTcRows - 1) / kTcRows;
+      const int64_t nseg = (nstage + p.seg - 1) / p.seg;
+      for (int64_t sg = 0; sg < nseg; ++sg, ++sc) {
+        const uint32_t tb = sc & 1u;
+        tc::wait(&acc_full[tb], (sc >> 1) & 1u);
+        tc::fence_after_sync();
+        const uint32_t sbuf = tmem + lanes + tb * uint32_t(cols_per_buf);
+        if (!(p.ablate & 4)) {
+          for (int c = 0; c < nchunk; ++c) {
+            uint32_t v[16], r[16];
+            tc::tmem_ld16_nowait(sbuf + uint32_t(c * 16), v);
+            if (sg > 0) tc::tmem_ld16_nowait(run + uint32_t(c * 16), r);
+            tc::tmem_ld_wait();
+            if (sg > 0) {
 #pragma unroll
-            for (int c0 = 0; c0 < N; c0 += 32) {
-              uint32_t v[32];
-              tc::tmem_ld32(tbase + uint32_t((s * p.mt + m) * N + c0), v);
-              // one 128-byte row segment per thread, 16-byte stores (columns
-              // R..RP-1 carry the zero B columns' G = 0)
-              float4* dst = reinterpret_cast<float4*>(p.partA + ((int64_t(s) * p.units + u) * K + k) * p.RP + c0);
-#pragma unroll
-              for (int r = 0; r < 32; r += 4)
-                if (c0 + r < p.RP)
-                  dst[r / 4] = make_float4(__uint_as_float(v[r]), __uint_as_float(v[r + 1]),
-                                           __uint_as_float(v[r + 2]), __uint_as_float(v[r + 3]));
+              for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(v[j]));
             }
+            tc::tmem_st16(run + uint32_t(c * 16), v);
+          }
+          tc::tmem_st_wait();
+        }
+        tc::fence_before_sync();
+        tc::arrive(&acc_empty[tb]);
+      }
+      if (p.ablate & 4) continue;
+      if (p.caseA) {
+        for (int t = 0; t < ntile; ++t) {
+          const int s = t / p.mtw, m = t - s * p.mtw;
+          const int64_t k = int64_t(g * p.mtw + m) * 128 + quarter * 32 + lane;
+          // one row segment per thread, 16-byte stores (columns R..RP-1 carry
+          // the zero B columns' G = 0)
+          float4* dst = reinterpret_cast<float4*>(p.partA + ((int64_t(s) * p.units + u) * K + k) * p.RP);
+          for (int c = 0; c < N; c += 16) {
+            if (c >= p.RP) break;
+            uint32_t v[16];
+            tc::tmem_ld16_nowait(run + uint32_t(t * N + c), v);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int r = 0; r < 16; r += 4)
+              if (c + r < p.RP)
+                dst[(c + r) / 4] = make_float4(__uint_as_float(v[r]), __uint_as_float(v[r + 1]),
+                                               __uint_as_float(v[r + 2]), __uint_as_float(v[r + 3]));
           }
         }
       } else {
-        float acc[CW];
-        for (int step = 0; step < nsteps; ++step) {
-          const int m = step % p.mt;
-          const int c = (step / p.mt) % NC;
-          const int s = step / (p.mt * NC);
-          load_lf(step + 1 < nsteps ? step + 1 : 0, nxt);  // next step, or the next unit's first
-          if (m == 0) {
+        // per (stream, 16-column chunk): fp32 dot over this thread's k rows of
+        // the item's m-tiles, then a transposing butterfly over the 32 lanes
+        // (16 shuffles for 16 columns); lane l ends with column col(l)
+        const int col = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+        for (int s = 0; s < p.ns; ++s) {
+          for (int c = 0; c < N; c += 16) {
+            float a[16];
 #pragma unroll
-            for (int r = 0; r < CW; ++r) acc[r] = 0.f;
-          }
-          uint32_t v[32];
-          tc::tmem_ld32(tbase + uint32_t((s * p.mt + m) * N + c * CW), v);
-          const float* f = reinterpret_cast<const float*>(cur);
-          // fp32 over the <= 4 m-tiles of one k residue (G is an fp32 MMA
-          // result; the cross-k and cross-unit sums below are fp64)
+            for (int j = 0; j < 16; ++j) a[j] = 0.f;
+            for (int m = 0; m < p.mtw; ++m) {
+              const int t = s * p.mtw + m;
+              const int64_t k = int64_t(g * p.mtw + m) * 128 + quarter * 32 + lane;
+              const float4* f4 = reinterpret_cast<const float4*>((s ? p.lastfac[1] : p.lastfac[0]) + k * N + c);
+              uint32_t v[16];
+              tc::tmem_ld16_nowait(run + uint32_t(t * N + c), v);
+              float f[16];
 #pragma unroll
-          for (int r = 0; r < CW; ++r) acc[r] = fmaf(__uint_as_float(v[r]), f[r], acc[r]);
-          if (m == p.mt - 1) {
+              for (int j = 0; j < 4; ++j) {
+                const float4 q4 = __ldg(f4 + j);
+                f[4 * j] = q4.x; f[4 * j + 1] = q4.y; f[4 * j + 2] = q4.z; f[4 * j + 3] = q4.w;
+              }
+              tc::tmem_ld_wait();
 #pragma unroll
-            for (int r = 0; r < CW; ++r) {
-              const double w = warp_sum(double(acc[r]));
-              if (lane == 0) red[quarter][c * CW + r] = w;
+              for (int j = 0; j < 16; ++j) a[j] = fmaf(__uint_as_float(v[j]), f[j], a[j]);
             }
-            if (c == NC - 1) {
-              named_sync(1, 128);
-              if (et < p.R)
-                p.partB[((int64_t(s) * In + itgt) * p.S + split) * p.RP + et] =
-                    red[0][et] + red[1][et] + red[2][et] + red[3][et];
-              named_sync(1, 128);
-            }
-          }
 #pragma unroll
-          for (int j = 0; j < V4; ++j) cur[j] = nxt[j];
+            for (int lvl = 0; lvl < 4; ++lvl) {
+              const int msk = 16 >> lvl, half = 8 >> lvl;
+              const bool upper = (lane & msk) != 0;
+#pragma unroll
+              for (int i = 0; i < half; ++i) {
+                const float send = upper ? a[i] : a[i + half];
+                const float keep = upper ? a[i + half] : a[i];
+                a[i] = keep + __shfl_xor_sync(0xffffffffu, send, msk);
+              }
+            }
+            a[0] += __shfl_xor_sync(0xffffffffu, a[0], 1);
+            if ((lane & 1) == 0) red[quarter][s * N + c + col] = double(a[0]);
+          }
         }
+        named_sync(1, 128);
+        if (et < p.ns * N) {
+          const int s = et / N, r = et - s * N;
+          if (r < p.R)
+            p.partB[((int64_t(s) * In + itgt) * (p.S * p.G) + split * p.G + g) * p.RP + r] =
+                red[0][et] + red[1][et] + red[2][et] + red[3][et];
+        }
+        named_sync(1, 128);
       }
-      if (tr) tr[1] = clock64();
-      tc::fence_before_sync();
-      tc::arrive(&acc_empty[tb]);
     }
   }
   tc::fence_before_sync();

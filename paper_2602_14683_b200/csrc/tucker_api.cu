@@ -287,6 +287,48 @@ void tucker_objective(Context& c, int prec, double beta, uint32_t order, const u
   });
 }
 
+void tucker_jcomm_reference(Context& c, int prec, double beta, double eps, uint32_t order, const uint64_t* dims,
+                            const double* x, const uint64_t* ranks, const double* ref_core, const double* ref_factors,
+                            double* p_out, double* q_out) {
+  NTFG_TDISPATCH(prec, {
+    with_tucker<T>(c, order, dims, ranks, beta, eps, [&](TuckerEngine<T>& e) {
+      e.stream().set_x(x, 0, NTFG_HOST);
+      e.set_model_host(ref_core, ref_factors);
+      e.set_ref_host(ref_core, ref_factors);
+      e.stream().prealloc(2);
+      e.weights_of_ref();
+      const size_t E = size_t(e.stream().entries());
+      std::vector<T> h(E);
+      c.d2h(h.data(), e.stream().p(), E * sizeof(T));
+      c.sync();
+      for (size_t i = 0; i < E; ++i) p_out[i] = double(h[i]);
+      c.d2h(h.data(), e.stream().q_always(), E * sizeof(T));
+      c.sync();
+      for (size_t i = 0; i < E; ++i) q_out[i] = double(h[i]);
+    });
+  });
+}
+
+void tucker_jcomm_inner_update(Context& c, int prec, double beta, double eps, uint32_t order, const uint64_t* dims,
+                               const double* p, const double* q, const uint64_t* ranks, const double* ref_core,
+                               const double* ref_factors, double* core, double* factors, int32_t block) {
+  if (block >= int32_t(order)) throw Error(NTFG_ERR_SHAPE, "jcomm_inner_factor_update: mode out of range");
+  NTFG_TDISPATCH(prec, {
+    with_tucker<T>(c, order, dims, ranks, beta, eps, [&](TuckerEngine<T>& e) {
+      e.set_model_host(core, factors);
+      e.set_ref_host(ref_core, ref_factors);
+      e.stream().prealloc(2);
+      const size_t E = size_t(e.stream().entries());
+      upload_t<T>(c, e.stream().p(), p, E);
+      upload_t<T>(c, e.stream().q_always(), q, E);
+      e.chi_from_ref();
+      if (block < 0) e.jcomm_inner_core();
+      else e.jcomm_inner_factor(int(block));
+      e.get_model_host(core, factors);
+    });
+  });
+}
+
 void tucker_step(Context& c, int prec, int kind, double beta, double eps, uint64_t inner, uint32_t order,
                  const uint64_t* dims, const double* x, const uint64_t* ranks, const double* ref_core,
                  const double* ref_factors, double* core, double* factors, uint32_t mode) {

@@ -86,6 +86,18 @@ def attach_nccl(ctx, group=None):
     ctx.init_nccl(obj[0], dist.get_world_size(group), dist.get_rank(group))
 
 
+def shard_coo(indices, values, global_dim0: int, world: int, rank: int):
+    """Nonzero partition by mode-0 index ranges: this rank's
+    nonzeros with i_0 rebased to its slab, plus (row0, row1)."""
+    idx = np.asarray(indices)
+    val = np.asarray(values)
+    row0, row1 = slab_rows(global_dim0, world, rank)
+    keep = (idx[:, 0] >= row0) & (idx[:, 0] < row1)
+    local = idx[keep].astype(np.int32, copy=True)
+    local[:, 0] -= row0
+    return local, val[keep].copy(), (row0, row1)
+
+
 def gather_mode0(local: np.ndarray, global_dim0: int, group=None) -> np.ndarray:
     """All-gathers the mode-0 factor slabs into the full I_0 x R matrix."""
     import torch

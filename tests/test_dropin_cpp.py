@@ -32,7 +32,10 @@ def test_dropin_compiles_and_links(tmp_path):
                  "ntf::block_core_update", "ntf::block_factor_update", "ntf::tucker_bcomm_sweep",
                  "ntf::make_jcomm_tucker_reference", "ntf::jcomm_inner_core_update",
                  "ntf::jcomm_inner_factor_update", "ntf::jcomm_tucker_outer_step", "ntf::cp_reconstruct",
-                 "ntf::D_beta", "ntf::D_beta_mean", "ntf::validate_fit_config"]:
+                 "ntf::D_beta", "ntf::D_beta_mean", "ntf::validate_fit_config",
+                 "ntf::make_extrapolation_state", "ntf::extrapolation_begin_iteration", "ntf::extrapolate_block",
+                 "ntf::extrapolation_end_iteration", "ntf::make_tucker_extrapolation_state",
+                 "ntf::extrapolate_core"]:
         assert name + "(" in syms, name
 
 

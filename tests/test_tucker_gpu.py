@@ -77,7 +77,7 @@ def test_first_joint_core_update_equals_block_bitwise(beta, precision):
     """reference test_tucker.cpp:83-94."""
     x = O.random_tensor([5, 4, 3], 5)
     m = O.init_tucker_model([5, 4, 3], [2, 2, 2], 5, EPS)
-    ctx = ntf.make_jcomm_tucker_reference(m, x, beta, EPS)
+    ctx = ntf.make_jcomm_tucker_reference(m, x, beta, EPS, precision=precision)
     joint = ntf.jcomm_inner_core_update(m, ctx, beta, EPS, precision=precision)
     block = ntf.block_core_update(m, x, beta, EPS, precision=precision)
     assert np.array_equal(joint[0], block[0])
@@ -92,6 +92,8 @@ def test_joint_inner_updates_vs_oracle(beta):
            [a * (1 + 0.2 * rng.uniforms(a.size).reshape(a.shape)) for a in ref[1]])
     octx = O.make_jcomm_tucker_reference(ref, x, beta, EPS)
     ctx = ntf.make_jcomm_tucker_reference(ref, x, beta, EPS)
+    # the cache is the reference's type: host P~/Q~ (tucker.hpp:59-63)
+    assert O.rel_err(ctx.p, octx[1]) < 1e-12 and O.rel_err(ctx.q, octx[2]) < 1e-12
     got = ntf.jcomm_inner_core_update(cur, ctx, beta, EPS)
     assert rel_model(got, O.jcomm_inner_core_update(cur, octx, beta, EPS)) < 1e-12
     for n in range(3):

@@ -9,8 +9,6 @@ import sys
 
 if len(sys.argv) > 2:  # child
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    import torch
-    import bench
     import paper_2602_14683_b200 as ntf
     beta = float(sys.argv[1])
     if os.environ.get("WORKLOAD") == "c5":  # 4-way CP, R = 64 (C5 shape; dim from C5_DIM, default 256)
@@ -20,9 +18,10 @@ if len(sys.argv) > 2:  # child
         init = nio.cp_factors((d,) * 4, 64, seed=1, which="init")
         cfg = ntf.FitConfig(beta=beta, rank=64, inner_steps=5, max_iters=1, precision="f32", use_graphs=False)
     else:
-        x, init = bench.make_problem(bench.DIMS, bench.RANK, 0, 0, bench.DIMS[0], torch.device("cuda", 0))
-        cfg = ntf.FitConfig(beta=beta, rank=bench.RANK, inner_steps=bench.INNER, max_iters=3, precision="f32",
-                            use_graphs=False)
+        from paper_2602_14683_b200 import io as nio
+        x = nio.generate_cp_gamma((512,) * 3, 32, seed=0)
+        init = nio.cp_factors((512,) * 3, 32, seed=1, which="init")
+        cfg = ntf.FitConfig(beta=beta, rank=32, inner_steps=5, max_iters=3, precision="f32", use_graphs=False)
     ctx = ntf.default_context()
     ctx.set_profiling(True)
     try:
@@ -32,13 +31,16 @@ if len(sys.argv) > 2:  # child
     print(json.dumps(ctx.stats()))
 else:
     beta = sys.argv[1] if len(sys.argv) > 1 else "0.5"
-    for bits in [0, 1, 2, 4, 5, 6, 7, 3]:
+    variants = [(b, None) for b in [0, 1, 2, 4, 6, 3, 7]] + [(0, "100000"), (0, "4"), (0, "64")]
+    for bits, seg in variants:
         env = dict(os.environ, NTFG_TC_ABLATE=str(bits))
+        if seg:
+            env["NTFG_TC_SEG"] = seg
         out = subprocess.run([sys.executable, __file__, beta, "child"], env=env, capture_output=True, text=True)
         line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-300:]
         try:
             st = json.loads(line)
-            print(bits, "contract_ms/launch %.4f" % (st["contract_ms"] / max(st["contract_launches"], 1)),
+            print(os.environ.get("WORKLOAD", "c2"), bits, "seg", seg, "contract_ms/launch %.4f" % (st["contract_ms"] / max(st["contract_launches"], 1)),
                   "recon_ms", round(st["recon_ms"], 3))
         except Exception:
             print(bits, line)
