@@ -27,7 +27,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xcompiler", "-fvisibility=hidden", "-I" + INCLUDE, "-I" + CSRC]
-CU_SOURCES = ["cp_api.cu", "tucker_api.cu", "io_api.cu", "unfold_api.cu", "capi.cu"]
+CU_SOURCES = ["cp_api.cu", "tucker_api.cu", "io_api.cu", "unfold_api.cu", "capi.cu", "tc_contract.cu", "recon_tc.cu"]
 CXX_API_SOURCES = ["ntf_api.cpp"]
 
 
@@ -47,9 +47,17 @@ def _stale(target, deps):
 
 
 def _run(cmd):
+    import time
+    t0 = time.time()
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("build failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+    # stamp the output with the time the compile STARTED: a header edited while
+    # nvcc was running (minutes per file) must leave the object stale
+    if "-o" in cmd:
+        out = cmd[cmd.index("-o") + 1]
+        if os.path.exists(out):
+            os.utime(out, (t0, t0))
     return r
 
 

@@ -2,6 +2,7 @@
 // internal exceptions into status codes + a thread-local message; no C++
 // exception crosses this boundary.
 #include <cstdio>
+#include <cstring>
 #include <string>
 
 #include "engine.cuh"
@@ -71,7 +72,21 @@ void tucker_step(Context&, int, int, double, double, uint64_t, uint32_t, const u
 struct ntfg_context : ntfg::Context {};
 
 namespace {
-thread_local std::string g_last_error;
+// Thread-local last-error text in a trivially destructible buffer: callers may
+// reach the C ABI from their own thread_local destructors at thread exit (the
+// drop-in's per-thread context does), after a std::string here would already
+// have been destroyed.
+struct LastError {
+  char text[512];
+  void clear() { text[0] = '\0'; }
+  LastError& operator=(const char* s) {
+    std::strncpy(text, s ? s : "", sizeof(text) - 1);
+    text[sizeof(text) - 1] = '\0';
+    return *this;
+  }
+  const char* c_str() const { return text; }
+};
+thread_local LastError g_last_error = {{0}};
 
 template <class F>
 ntfg_status guard(F&& f) {

@@ -22,6 +22,7 @@
 #include "nccl_comm.cuh"
 #include "stream3_kernels.cuh"
 #include "recon_tile.cuh"
+#include "recon_tc.cuh"
 #include "tc_contract.cuh"
 
 namespace ntfg {
@@ -248,6 +249,22 @@ class CpEngine {
     const bool tile = tc_ && sizeof(T) == 4 && !htab && !xhout && !pout && !qout && rows_tma_ok(x_) &&
                       g_.K % kRtCols == 0 && RP_ <= 64 && !tile_disabled();
     obj_split_ = tile ? split_objective() : (planes_out_ && split_objective());
+    if (tile && recon_tc_ok()) {
+      // Xhat on the tensor cores (recon_tc.cuh): one persistent CTA per SM,
+      // grid a multiple of the k tiles
+      p.ktiles = int(g_.K / kRcCols);
+      const int64_t ntiles = g_.rows / kRcRows;
+      const int64_t per = std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(c_.sm_count) / p.ktiles));
+      recon_grid_ = int(per * p.ktiles);
+      const int ph = c_.prof_begin(0);
+      if constexpr (sizeof(T) == 4) {
+        recon_tc_launch(recon_grid_, c_.stream, p, RP_, bk_);
+        NTFG_LAUNCHED(c_);
+      }
+      c_.prof_end(ph);
+      if (objective) finish_objective();
+      return;
+    }
     if (tile) {
       p.ktiles = int(g_.K / kRtCols);
       const int ph = c_.prof_begin(0);
@@ -323,12 +340,12 @@ class CpEngine {
   // shared-memory plan of one contraction launch: A stages (1024-aligned),
   // B tiles, then the B producers' cp.async gather ring.  Deeper gathers first
   // (they hide the L2 latency of the factor rows), then more stages.
-  // m-tiles per work item: the epilogue keeps ns * mtw * N fp32 segment sums
-  // per thread in registers (<= 128)
+  // m-tiles per work item: ns * mtw * N segment accumulator columns plus as
+  // many running-sum columns must fit the 512 TMEM columns
   int tc_mtw(int ns) const {
     const int mt = int(g_.K / 128), N = tc_n();
     int w = mt;
-    while (w > 1 && (ns * w * N > 128 || mt % w != 0)) --w;
+    while (w > 1 && (ns * w * N > 256 || mt % w != 0)) --w;
     return w;
   }
   TcLayout tc_layout(int ns, int N, int nmm) const {
@@ -353,19 +370,6 @@ class CpEngine {
     L.ring_off = L.b_off + uint32_t(nst) * 4 * L.b_tile;
     L.total = uint32_t(total(nst, gd));
     return L;
-  }
-  template <typename KF>
-  void launch_tc(KF kern, int grid, const TcMaps& maps, const TcParams& p) {
-    static std::mutex mu;
-    static std::set<const void*> done;
-    {
-      std::lock_guard<std::mutex> lock(mu);
-      if (done.insert(reinterpret_cast<const void*>(kern)).second)
-        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemMax)),
-                   "cudaFuncSetAttribute");
-    }
-    kern<<<grid, p.N <= 32 ? tc_threads<32>() : tc_threads<64>(), p.lay.total, c_.stream>>>(maps, p);
-    NTFG_LAUNCHED(c_);
   }
   bool tc() const { return tc_; }
   void disable_tc() { tc_allowed_ = false; tc_ = false; }
@@ -478,9 +482,9 @@ class CpEngine {
     }
     p.partA = reinterpret_cast<float*>(partA_);
     p.partB = partB_;
-    const int cols = ns * p.mtw * p.N;  // one segment buffer; two alternate, plus the running sums
+    const int cols = ns * p.mtw * p.N;  // segment accumulators, then the running sums
     int alloc = 32;
-    while (alloc < 3 * cols) alloc *= 2;
+    while (alloc < 2 * cols) alloc *= 2;
     p.tmem_cols = alloc;
     p.items = p.units * p.G;
     {  // perf experiments only (tools/): role ablation bits, results are wrong when set
@@ -493,9 +497,8 @@ class CpEngine {
       p.trace = reinterpret_cast<unsigned long long*>(c_.bufs.get("cp.tctrace", size_t(grid) * 17 * 8 * 8));
       NTFG_CUDA(cudaMemsetAsync(p.trace, 0, size_t(grid) * 17 * 8 * 8, c_.stream));
     }
-    if (p.N == 16) launch_tc(tc_contract_kernel<16>, grid, maps, p);
-    else if (p.N == 32) launch_tc(tc_contract_kernel<32>, grid, maps, p);
-    else launch_tc(tc_contract_kernel<64>, grid, maps, p);
+    tc_contract_launch(grid, c_.stream, maps, p);
+    NTFG_LAUNCHED(c_);
     if (trace_path) {
       std::vector<unsigned long long> h(size_t(grid) * 17 * 8);
       NTFG_CUDA(cudaMemcpyAsync(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost, c_.stream));
@@ -1172,6 +1175,13 @@ class CpEngine {
     NTFG_LAUNCHED(c_);
   }
 
+  // tcgen05 reconstruction: the fastest row mode has 128 | I (a 128-row tile
+  // then shares the slower coordinates), K = 128..512 in 128 steps
+  bool recon_tc_ok() const {
+    static const bool off = [] { const char* e = std::getenv("NTFG_DISABLE_RECON_TC"); return e && e[0] == '1'; }();
+    return !off && N_ >= 2 && g_.dims[N_ - 2] % kRcRows == 0 && g_.small_rows && g_.K % kRcCols == 0 &&
+           g_.K / kRcCols <= 4;
+  }
   static bool tile_disabled() {  // perf experiments: NTFG_DISABLE_RTILE=1 keeps recon3
     static const bool v = [] { const char* e = std::getenv("NTFG_DISABLE_RTILE"); return e && e[0] == '1'; }();
     return v;

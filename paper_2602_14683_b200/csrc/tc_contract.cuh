@@ -42,6 +42,7 @@ namespace ntfg {
 constexpr int kTcRows = 16;     // UMMA K for 16-bit inputs
 constexpr int kTcMaxStages = 6;
 constexpr int kTcMaxGather = 6;
+constexpr int kTcMaxTiles = 8;   // accumulator tiles per work item: ns * mtw
 // MMA-issuing warps (9, and 11 when 2): one issuing thread was the stage-rate
 // limit at N <= 32 (C2 K3 0.198 -> 0.189 ms); at N = 64 a second issuer gains
 // nothing and its registers push the kernel into spills, so it stays at one
@@ -102,18 +103,28 @@ __device__ __forceinline__ void bf16_split(double v, __nv_bfloat16& hi, __nv_bfl
   lo = __float2bfloat16_rn(f - __bfloat162float(hi));
 }
 
+// The kernel lives in its own translation unit (tc_contract.cu); the engine
+// launches it through this entry point (sets the dynamic shared-memory
+// attribute once per instance).
+void tc_contract_launch(int grid, cudaStream_t stream, const TcMaps& maps, const TcParams& p);
+
+#ifdef NTFG_TC_CONTRACT_IMPL
 template <int NMAX>
 static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     tc_contract_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   const TcLayout& L = p.lay;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t a_full[kTcMaxStages], b_full[kTcMaxStages], empty[kTcMaxStages], acc_full[2], acc_empty[2];
+  __shared__ uint64_t a_full[kTcMaxStages], b_full[kTcMaxStages], empty[kTcMaxStages];
+  __shared__ uint64_t acc_full[kTcMaxTiles], acc_empty[kTcMaxTiles];  // per accumulator tile (stream, m-tile)
   __shared__ uint64_t g_full[kTcMaxGather], g_empty[kTcMaxGather];
   __shared__ uint32_t tmem_base;
   __shared__ double red[4][128];
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // warp index through a shuffle: the compiler then treats the role branches
+  // (and everything computed inside them from uniform inputs) as warp-uniform
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int64_t K = p.g.K;
   const int64_t In = p.g.dims[p.n];
   constexpr int N = NMAX;  // UMMA N (host launches the instance matching the rank)
@@ -128,9 +139,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
       tc::mbar_init(&g_full[g], 1);
       tc::mbar_init(&g_empty[g], 128);
     }
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&acc_full[b], tc_issuers<NMAX>());
-      tc::mbar_init(&acc_empty[b], 128);
+    for (int t = 0; t < kTcMaxTiles; ++t) {
+      tc::mbar_init(&acc_full[t], 1);     // committed by the tile's issuer
+      tc::mbar_init(&acc_empty[t], 128);  // drained by the epilogue threads
     }
   }
   tc::fence_barrier_init();
@@ -144,7 +155,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = tmem_base;
-  const int cols_per_buf = p.ns * p.mtw * N;  // one accumulation segment buffer (<= 128 columns)
+  const int cols_per_buf = p.ns * p.mtw * N;  // segment accumulators (<= 256 columns); the running sums follow
 
   auto unit_range = [&](int64_t u, int64_t& j0, int64_t& j1, int64_t& itgt, int64_t& split) {
     if (p.caseA) {
@@ -174,8 +185,11 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
 
   if (warp == 8) {
     // ================= TMA producer =================
-    if (lane == 0) {
-      uint32_t q = 0;
+    // converged warp, one elected lane issues (uniform operands: no per-lane
+    // operand marshalling around the TMA instructions)
+    {
+      int slot = 0;
+      uint32_t sph = 1;  // producer parity: the first pass over the ring finds every slot free
       const unsigned bytes = unsigned(p.ns) * 2u * unsigned(2 * p.mtw) * 2048u;
       unsigned long long tw = 0, t00 = p.trace ? clock64() : 0;
       for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
@@ -183,12 +197,10 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         const int blk0 = int(w % p.G) * 2 * p.mtw;  // first 64-column block of this item's m-tiles
         int64_t j0, j1, itgt, split;
         unit_range(u, j0, j1, itgt, split);
-        for (int64_t j = j0; j < j1; j += kTcRows, ++q) {
-          const int slot = int(q % unsigned(L.nst));
+        for (int64_t j = j0; j < j1; j += kTcRows) {
           const unsigned long long tq = p.trace ? clock64() : 0;
-          tc::wait(&empty[slot], ((q / unsigned(L.nst)) & 1u) ^ 1u);
+          tc::wait(&empty[slot], sph);
           if (p.trace) tw += clock64() - tq;
-          tc::expect_tx(&a_full[slot], bytes);
           int c2, c3, c4;
           if (p.caseA) {
             c2 = int(j); c3 = 0; c4 = 0;
@@ -196,12 +208,20 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
             const int64_t aa = p.g.small_rows ? p.fB.div(j) : j / p.Bn;
             c2 = int(j - aa * p.Bn); c3 = int(itgt); c4 = int(aa);
           }
-          for (int s = 0; s < p.ns; ++s)
-            for (int plane = 0; plane < 2; ++plane)
-              tc::tma_load_5d(stage_a(slot, s, plane), &maps.m[s][plane], 0, c2, c3, c4, blk0, &a_full[slot]);
+          if (tc::elect_one()) {
+            tc::expect_tx(&a_full[slot], bytes);
+            for (int s = 0; s < p.ns; ++s)
+              for (int plane = 0; plane < 2; ++plane)
+                tc::tma_load_5d(stage_a(slot, s, plane), &maps.m[s][plane], 0, c2, c3, c4, blk0, &a_full[slot]);
+          }
+          __syncwarp();
+          if (++slot == L.nst) {
+            slot = 0;
+            sph ^= 1u;
+          }
         }
       }
-      if (p.trace) {
+      if (p.trace && lane == 0) {
         p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 5] = tw;
         p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 6] = clock64() - t00;
       }
@@ -209,54 +229,72 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   } else if (warp == 9 || (warp == 11 && tc_issuers<NMAX>() > 1)) {
     // ================= MMA issuers =================
     // issuer i (warp 9: 0, warp 11: 1) owns the accumulator tiles t = s * mtw + m
-    // with t % 2 == i; each commits every stage slot and segment buffer
-    // (barrier counts kTcIssuers).  The accumulator restarts from zero every
-    // p.seg stages (a "segment", alternating between two TMEM buffers) and the
-    // epilogue adds the segment sums on the CUDA cores: long fp32 accumulation
-    // chains inside the tensor core drift low (measured: C2 beta = 1 factors
-    // 1.3e-3 off the fp64 build after 100 outer iterations with 111-stage
-    // chains, 3.5e-5 with 16-stage chains), the CUDA-core sums round to nearest.
+    // with t % 2 == i.  The accumulator of a tile restarts from zero every
+    // p.seg stages (a "segment"); the epilogue adds each finished segment into
+    // running sums (a second TMEM region) on the CUDA cores: long fp32
+    // accumulation chains inside the tensor core drift low (measured: C2
+    // beta = 1 factors 1.3e-3 off the fp64 build after 100 outer iterations
+    // with 111-stage chains, 3.5e-5 with 16-stage chains), the CUDA-core sums
+    // round to nearest.  One segment buffer: tile t's drain overlaps the last
+    // stage's MMAs of tiles t+1.. (per-tile full/empty barriers).
+    //
+    // The whole warp runs this loop converged and every operand is a
+    // warp-uniform value (kernel parameters, loop counters, the smem base), so
+    // the MMAs issue from uniform registers; a single-lane (divergent) issuer
+    // makes the compiler wrap every tcgen05.mma in an elect/R2UR loop, which
+    // cost ~150 cycles per MMA against the 43 + N/2 the tensor pipe needs
+    // (tools/mma_probe.cu).
     const int issuer = warp == 9 ? 0 : 1;
-    if (lane == 0) {
-      const uint32_t idesc = tc::idesc_bf16_f32(128, N, true, false);
-      const int ntile = p.ns * p.mtw;
-      uint32_t q = 0, sc = 0;
-      for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
-        int64_t j0, j1, itgt, split;
-        unit_range(w / p.G, j0, j1, itgt, split);
-        uint32_t tb = 0;
-        bool first = true;
-        int qi = 0;
-        for (int64_t j = j0; j < j1; j += kTcRows, ++q, ++qi) {
-          if (qi == 0) {  // segment start: wait until the epilogue drained this buffer
-            tb = sc & 1u;
-            tc::wait(&acc_empty[tb], ((sc >> 1) & 1u) ^ 1u);
+    const uint32_t idesc = tc::idesc_bf16_f32(128, N, true, false);
+    const int ntile = p.ns * p.mtw;
+    const uint64_t a_desc0 = tc::desc_mn_sw128(smem, 2048, 1024);
+    const uint64_t b_desc0 = tc::desc_k_interleave(smem + L.b_off, 128, kTcBSbo);
+    const uint32_t a_plane16 = (L.a_stream / 2) >> 4, b_tile16 = L.b_tile >> 4;
+    int slot = 0;
+    uint32_t sph = 0, sc = 0;
+    for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
+      int64_t j0, j1, itgt, split;
+      unit_range(w / p.G, j0, j1, itgt, split);
+      const int nstage = int((j1 - j0 + kTcRows - 1) / kTcRows);
+      int qi = 0;
+      for (int stg = 0; stg < nstage; ++stg) {
+        const bool seg_first = qi == 0;
+        const bool seg_last = qi == p.seg - 1 || stg == nstage - 1;
+        tc::wait(&a_full[slot], sph);
+        tc::wait(&b_full[slot], sph);
+        tc::fence_after_sync();
+        for (int t = issuer; t < ntile; t += tc_issuers<NMAX>()) {
+          const int s = t >= p.mtw ? 1 : 0, m = t - s * p.mtw;
+          if (seg_first) {  // the epilogue drained this tile's previous segment
+            tc::wait(&acc_empty[t], (sc & 1u) ^ 1u);
             tc::fence_after_sync();
-            first = true;
           }
-          const int slot = int(q % unsigned(L.nst));
-          const uint32_t ph = (q / unsigned(L.nst)) & 1u;
-          tc::wait(&a_full[slot], ph);
-          tc::wait(&b_full[slot], ph);
-          tc::fence_after_sync();
-          for (int t = issuer; t < ntile && !(p.ablate & 2); t += tc_issuers<NMAX>()) {
-            const int s = t / p.mtw, m = t - s * p.mtw;
-            const uint64_t bh = tc::desc_k_interleave(stage_b(slot, s, 0), 128, kTcBSbo);
-            const uint64_t bl = tc::desc_k_interleave(stage_b(slot, s, 1), 128, kTcBSbo);
-            const uint32_t d = tmem + tb * uint32_t(cols_per_buf) + uint32_t(t * N);
-            const uint64_t ah = tc::desc_mn_sw128(stage_a(slot, s, 0) + size_t(m) * 4096, 2048, 1024);
-            const uint64_t al = tc::desc_mn_sw128(stage_a(slot, s, 1) + size_t(m) * 4096, 2048, 1024);
-            tc::mma_bf16(d, ah, bh, idesc, !first);
-            tc::mma_bf16(d, ah, bl, idesc, true);
-            tc::mma_bf16(d, al, bh, idesc, true);
+          const uint32_t aoff = uint32_t(slot) * L.a_stage + uint32_t(s) * L.a_stream + uint32_t(m) * 4096u;
+          const uint32_t boff = uint32_t((slot * 2 + s) * 2) * L.b_tile;
+          const uint64_t ah = a_desc0 + (aoff >> 4), al = ah + a_plane16;
+          const uint64_t bh = b_desc0 + (boff >> 4), bl = bh + b_tile16;
+          const uint32_t d = tmem + uint32_t(t * N);
+          if (tc::elect_one()) {
+            if (!(p.ablate & 2)) {
+              tc::mma_bf16(d, ah, bh, idesc, !seg_first);
+              tc::mma_bf16(d, ah, bl, idesc, true);
+              tc::mma_bf16(d, al, bh, idesc, true);
+            }
+            if (seg_last) tc::commit(&acc_full[t]);
           }
-          tc::commit(&empty[slot]);
-          first = false;
-          if (qi == p.seg - 1 || j + kTcRows >= j1) {  // segment end
-            tc::commit(&acc_full[tb]);
-            ++sc;
-            qi = -1;
-          }
+          __syncwarp();
+        }
+        if (tc::elect_one()) tc::commit(&empty[slot]);
+        __syncwarp();
+        if (++slot == L.nst) {
+          slot = 0;
+          sph ^= 1u;
+        }
+        if (seg_last) {
+          ++sc;
+          qi = 0;
+        } else {
+          ++qi;
         }
       }
     }
@@ -424,7 +462,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   } else {
     // ================= epilogue (warps 4..7: TMEM lane quarter = warp % 4) =================
     // Per segment: this thread's k row (lane) of the segment buffer is added
-    // into a running-sum region of TMEM (columns 2 * cols_per_buf ..) with
+    // into a running-sum region of TMEM (columns cols_per_buf ..) with
     // CUDA-core fp32 adds (round to nearest; tcgen05.ld -> FADD -> tcgen05.st).
     // Per work item: case A writes the [K][RP] partial of its m-tile group;
     // case B dots G with the last-mode factor over k: out(r) = sum_k
@@ -432,9 +470,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     const int quarter = warp & 3;
     const int et = tid - 128;  // 0..127
     const int ntile = p.ns * p.mtw;
-    const int nchunk = ntile * N / 16;
     const uint32_t lanes = uint32_t(quarter * 32) << 16;
-    const uint32_t run = tmem + lanes + 2u * uint32_t(cols_per_buf);
+    const uint32_t run = tmem + lanes + uint32_t(cols_per_buf);
+    const uint32_t sbuf = tmem + lanes;
     uint32_t sc = 0;
     for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
       const int64_t u = w / p.G;
@@ -444,26 +482,26 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
       const int64_t nstage = (j1 - j0 + kTcRows - 1) / kTcRows;
       const int64_t nseg = (nstage + p.seg - 1) / p.seg;
       for (int64_t sg = 0; sg < nseg; ++sg, ++sc) {
-        const uint32_t tb = sc & 1u;
-        tc::wait(&acc_full[tb], (sc >> 1) & 1u);
-        tc::fence_after_sync();
-        const uint32_t sbuf = tmem + lanes + tb * uint32_t(cols_per_buf);
-        if (!(p.ablate & 4)) {
-          for (int c = 0; c < nchunk; ++c) {
-            uint32_t v[16], r[16];
-            tc::tmem_ld16_nowait(sbuf + uint32_t(c * 16), v);
-            if (sg > 0) tc::tmem_ld16_nowait(run + uint32_t(c * 16), r);
-            tc::tmem_ld_wait();
-            if (sg > 0) {
+        for (int t = 0; t < ntile; ++t) {
+          tc::wait(&acc_full[t], sc & 1u);
+          tc::fence_after_sync();
+          if (!(p.ablate & 4)) {
+            for (int c = t * (N / 16); c < (t + 1) * (N / 16); ++c) {
+              uint32_t v[16], r[16];
+              tc::tmem_ld16_nowait(sbuf + uint32_t(c * 16), v);
+              if (sg > 0) tc::tmem_ld16_nowait(run + uint32_t(c * 16), r);
+              tc::tmem_ld_wait();
+              if (sg > 0) {
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(v[j]));
+                for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(v[j]));
+              }
+              tc::tmem_st16(run + uint32_t(c * 16), v);
             }
-            tc::tmem_st16(run + uint32_t(c * 16), v);
           }
-          tc::tmem_st_wait();
+          tc::fence_before_sync();
+          tc::arrive(&acc_empty[t]);  // the segment tile is read: its next segment may start
         }
-        tc::fence_before_sync();
-        tc::arrive(&acc_empty[tb]);
+        tc::tmem_st_wait();
       }
       if (p.ablate & 4) continue;
       if (p.caseA) {
@@ -541,6 +579,8 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   __syncthreads();
   if (warp == 9) tc::tmem_dealloc(tmem, uint32_t(p.tmem_cols));
 }
+
+#endif  // NTFG_TC_CONTRACT_IMPL
 
 // every factor of every stream, [I_m][R] fp64 -> [I_m][N] fp32 zero padded:
 // the B-operand gathers and the case-B epilogue's last factor (16-byte loads)

@@ -59,7 +59,24 @@ static CpFactors init(const std::vector<std::size_t>& dims, std::size_t r, unsig
     return CpFactors(f);
 }
 
-int main() {
+static int run();
+static const char* only = nullptr;  // debugging: run one stage (argv[1])
+static bool want(const char* name) { return !only || std::string(only) == name; }
+static const char* stage = "start";
+int main(int argc, char** argv) {
+    if (argc > 1) only = argv[1];
+    std::setvbuf(stdout, nullptr, _IONBF, 0);
+    try {
+        return run();
+    } catch (const std::exception& e) {
+        std::printf("EXCEPTION in stage '%s': %s\n", stage, e.what());
+        return 2;
+    }
+}
+
+static int run() {
+    stage = "kat";
+    std::printf("stage %s\n", stage);
     // reconstruct KAT (test_cp.cpp:22-33)
     CpFactors rank1({Matrix(2, 1, {1.0, 2.0}), Matrix(2, 1, {3.0, 4.0})});
     CHECK(cp_reconstruct(rank1).values() == std::vector<double>({3.0, 4.0, 6.0, 8.0}));
@@ -71,7 +88,10 @@ int main() {
     CHECK(g.factors[0](0, 0) == 2.0);
     CHECK(D_beta(x1, cp_reconstruct(g), kl) == 0.0);
 
+    stage = "first-inner";
+    std::printf("stage %s\n", stage);
     // first joint inner update == block update, bitwise (test_cp.cpp:116-128)
+    if (want("first-inner"))
     for (double b : {0.0, 0.5, 1.0, 1.5}) {
         const DenseTensor x = data({6, 5, 4}, 3);
         const CpFactors f = init(x.shape(), 2, 3);
@@ -81,7 +101,10 @@ int main() {
               bcomm_block_update(f, 0, x, p, 1e-12).factors[0].values());
     }
 
+    stage = "fit-drivers";
+    std::printf("stage %s\n", stage);
     // fit drivers: stopping rules, monotone traces (test_cp.cpp:88-114)
+    if (want("fit-drivers"))
     {
         const DenseTensor x = data({8, 7, 6}, 5);
         FitConfig cfg;
@@ -105,7 +128,10 @@ int main() {
         }
     }
 
+    stage = "errors";
+    std::printf("stage %s\n", stage);
     // error behaviour (config.cpp:7-18, fit_common.hpp:14-23)
+    if (want("errors"))
     {
         FitConfig bad;
         bad.beta = 2.0;
@@ -126,7 +152,10 @@ int main() {
         CHECK(named);
     }
 
+    stage = "tucker";
+    std::printf("stage %s\n", stage);
     // Tucker: core KAT and joint descent (test_tucker.cpp:21-29, 96-115)
+    if (want("tucker"))
     {
         const DenseTensor x = DenseTensor::full({2, 2}, 1.0);
         TuckerModel m(DenseTensor({1, 1}, {2.0}), {Matrix::full(2, 1, 1.0), Matrix::full(2, 1, 1.0)});
@@ -153,9 +182,12 @@ int main() {
         CHECK(r.trace.size() == 31);
     }
 
+    stage = "bmme";
+    std::printf("stage %s\n", stage);
     // BMMe step-level API (cp.hpp:80-110): a hand-written extrapolated B-CoMM
     // loop equals bcomm_fit(extrapolate) (reference test_cp.cpp:169-216 style);
     // cap = 0 pins alpha to 0 (test_cp.cpp:218-234)
+    if (want("bmme"))
     {
         const DenseTensor x = data({6, 5, 4}, 31);
         const BetaParam p(0.5);
@@ -185,14 +217,17 @@ int main() {
         extrapolation_begin_iteration(z, f);
         CHECK(z.alpha == 0.0);
         CHECK(extrapolate_block(f.factors[0], z, 0).values() == f.factors[0].values());
-        TuckerModel tm(DenseTensor::full({2, 2, 2}, 0.7), f.factors);
+        TuckerModel tm(DenseTensor::full({3, 3, 3}, 0.7), f.factors);
         TuckerExtrapolationState ts = make_tucker_extrapolation_state(tm, true, 1.0, 1e-6, 1e-12);
         extrapolation_begin_iteration(ts, tm);
         CHECK(extrapolate_core(tm.core, ts).values() == tm.core.values());
     }
 
+    stage = "tucker-cache";
+    std::printf("stage %s\n", stage);
     // Tucker joint-MM cache holds host P~/Q~ (tucker.hpp:59-63); first inner
     // core update == block core update (test_tucker.cpp:83-94)
+    if (want("tucker-cache"))
     {
         const DenseTensor y = data({5, 4, 3}, 41);
         const CpFactors f = init(y.shape(), 2, 41);

@@ -101,3 +101,53 @@ def test_tc_fast_and_generic_gathers_agree(dims, monkeypatch):
     monkeypatch.setenv("NTFG_TC_SLOW_GATHER", "1")
     b = ntf.jcomm_fit(x, init, cfg)
     assert all(np.array_equal(u, v) for u, v in zip(a.model, b.model))
+
+
+# Shapes that take the tcgen05 reconstruction (recon_tc.cuh): the fastest row
+# mode a multiple of 128, K = 128..512; every rank padding (8/16/32/64), 2-, 3-
+# and 4-way tensors, all beta kinds incl. the generic power (beta = 1.3).
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 1.3, 1.5])
+@pytest.mark.parametrize("dims,rank", [((3, 128, 128), 5), ((2, 256, 256), 12), ((128, 384), 20),
+                                       ((2, 3, 128, 128), 40), ((5, 128, 512), 64)])
+def test_recon_tc_fit_matches_oracle(beta, dims, rank):
+    x, init = problem(dims, rank, 17)
+    cfg = ntf.FitConfig(beta=beta, rank=rank, max_iters=6, inner_steps=2, precision="f32")
+    res = ntf.jcomm_fit(x, init, cfg)
+    om, otr = O.jcomm_fit(x, init, O.FitConfig(beta=beta, rank=rank, max_iters=6, inner_steps=2))
+    assert relm(res.model, om) < 1e-4
+    assert O.rel_err([t.loss for t in res.trace], [t[2] for t in otr]) < 1e-5
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 1.5])
+def test_recon_tc_planes_and_objective_vs_tile_kernel(beta, monkeypatch):
+    # same P~/Q~ planes (to the hi/lo plane resolution) and objective as the
+    # CUDA-core tile kernel (NTFG_DISABLE_RECON_TC=1 is read once per process,
+    # so compare against the oracle instead: planes 2e-5, objective 1e-6)
+    x, f = problem((2, 128, 256), 24, 19)
+    ctx = ntf.make_jcomm_reference(f, x, beta, EPS, precision="f32")
+    _, op, oq = O.make_jcomm_reference(f, x, beta, EPS)
+    assert O.rel_err(ctx.p / np.maximum(op, 1e-30), np.ones_like(op)) < 2e-5
+    if beta != 1.0:
+        assert O.rel_err(ctx.q / oq, np.ones_like(oq)) < 2e-5
+    res = ntf.jcomm_fit(x, f, ntf.FitConfig(beta=beta, rank=24, max_iters=1, inner_steps=1, precision="f32"))
+    want = O.D_beta_mean(x, O.cp_reconstruct(f), beta)
+    assert abs(res.trace[0].loss - want) <= 1e-6 * max(1.0, abs(want))
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 1.5])
+def test_recon_tc_first_joint_inner_equals_block_bitwise(beta):
+    x, f = problem((2, 128, 128), 6, 21)
+    ctx = ntf.make_jcomm_reference(f, x, beta, EPS, precision="f32")
+    for mode in range(3):
+        joint = ntf.jcomm_inner_update(f, ctx, mode, beta, EPS, precision="f32")
+        block = ntf.bcomm_block_update(f, mode, x, beta, EPS, precision="f32")
+        assert np.array_equal(joint[mode], block[mode]), mode
+
+
+def test_recon_tc_data_floor_and_domain_flags():
+    # zero data at beta = 0 -> infinite objective -> NumericalError naming the data floor,
+    # through the tcgen05 reconstruction's exact per-entry fallback
+    x, f = problem((2, 128, 128), 4, 23)
+    x[0, 5, 7] = 0.0
+    with pytest.raises(ntf.NumericalError, match="data-floor"):
+        ntf.jcomm_fit(x, f, ntf.FitConfig(beta=0.0, rank=4, max_iters=2, precision="f32"))
