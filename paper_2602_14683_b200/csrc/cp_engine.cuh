@@ -348,21 +348,35 @@ class CpEngine {
     while (w > 1 && (ns * w * N > 256 || mt % w != 0)) --w;
     return w;
   }
-  TcLayout tc_layout(int ns, int N, int nmm) const {
+  TcLayout tc_layout(int ns, int N, int nmm, bool gfast) const {
     TcLayout L{};
     L.a_stream = uint32_t(2 * (2 * tc_mtw(ns)) * 2048);
     L.a_stage = uint32_t(ns) * L.a_stream;
     L.b_tile = uint32_t(N / 8 * kTcBSbo);
     L.gmodes = std::max(1, std::min(nmm, kTcGModes));
-    const size_t ring_per = size_t(ns) * L.gmodes * 16 * N * 4;  // [slot][ns][gmodes][16 rows][N]
+    // gather slot: per stream gm regions of [16][N] floats, or (fast path) one
+    // [16][N] region plus one row per other mode
+    L.g_stream = gfast ? uint32_t(16 + L.gmodes - 1) * uint32_t(N * 4) : uint32_t(L.gmodes) * 16u * uint32_t(N * 4);
+    L.g_slot = uint32_t(ns) * L.g_stream;
     auto total = [&](int nst, int gd) {
-      return size_t(nst) * L.a_stage + size_t(nst) * 4 * L.b_tile + size_t(gd) * ring_per + 1024;
+      return size_t(nst) * L.a_stage + size_t(nst) * 4 * L.b_tile + size_t(gd) * L.g_slot + 1024;
     };
-    int nst = 3, gd = 2;
-    if (total(nst, gd) > kTcSmemMax) nst = 2;
-    while (gd < 4 && total(nst, gd + 1) <= kTcSmemMax) ++gd;
-    static_assert(kTcMaxGather >= 4, "gather ring depth");
+    // Stages first: the A stages are the HBM bytes in flight (a C5 stage is
+    // 32 KB; three of them per SM are below the ~90 KB the bandwidth-latency
+    // product asks for), then gather depth (L2 latency of the factor rows).
+    static const int env_nst = [] { const char* e = std::getenv("NTFG_TC_NST"); return e ? std::atoi(e) : 0; }();
+    static const int env_gd = [] { const char* e = std::getenv("NTFG_TC_GD"); return e ? std::atoi(e) : 0; }();
+    int gd = 2, nst = 2;
     while (nst < kTcMaxStages && total(nst + 1, gd) <= kTcSmemMax) ++nst;
+    // give one stage back for gather depth only when more than four stages fit
+    while (gd < 4 && total(nst, gd + 1) <= kTcSmemMax) ++gd;
+    if (gd < 3 && nst > 4 && total(nst - 1, 3) <= kTcSmemMax) {
+      --nst;
+      gd = 3;
+      while (gd < 4 && total(nst, gd + 1) <= kTcSmemMax) ++gd;
+    }
+    if (env_nst > 0) nst = std::min(env_nst, kTcMaxStages);
+    if (env_gd > 0) gd = std::min(env_gd, kTcMaxGather);
     if (total(nst, gd) > kTcSmemMax) throw Error(NTFG_ERR_SHAPE, "tensor-core contraction: shared memory plan");
     L.nst = nst;
     L.gdepth = gd;
@@ -402,6 +416,24 @@ class CpEngine {
     for (int m = n + 1; m < N_ - 1; ++m) Bn *= g_.dims[m];
     const int64_t tot = An * Bn;
     int64_t S0 = std::max<int64_t>(1, std::min<int64_t>(ceil_div(int64_t(4) * c_.sm_count, In), ceil_div(tot, kTcRows)));
+    {
+      // units are dealt round-robin to one CTA per SM: pick the split count in
+      // [S0, S0 + 8] whose last wave is fullest (C5: S = 3 gives 768 units =
+      // 5.19 waves, i.e. 6 -- 13% of the launch idle; S = 4 gives 6.92 -> 7)
+      const int64_t smax = std::min<int64_t>(S0 + 8, std::max<int64_t>(S0, tot / (4 * kTcRows)));
+      double best = 0.0;
+      int64_t bestS = S0;
+      for (int64_t s = S0; s <= smax; ++s) {
+        const int64_t chunk_s = ceil_div(ceil_div(tot, s), kTcRows) * kTcRows;
+        const int64_t units_s = In * ceil_div(tot, chunk_s);
+        const double eff = double(units_s) / double(ceil_div(units_s, c_.sm_count) * c_.sm_count);
+        if (eff > best + 0.01) {
+          best = eff;
+          bestS = s;
+        }
+      }
+      S0 = bestS;
+    }
     if (cap > 0) S0 = std::max(S0, ceil_div(tot, ceil_div(cap, kTcRows) * kTcRows));
     chunk = ceil_div(ceil_div(tot, S0), kTcRows) * kTcRows;
     S = ceil_div(tot, chunk);
@@ -471,7 +503,6 @@ class CpEngine {
     NTFG_LAUNCHED(c_);
     int nmm = 0;
     for (int m = 0; m < N_ - 1; ++m) nmm += (m != n);
-    p.lay = tc_layout(ns, p.N, nmm);
     {  // fast gathers: the fastest off-mode f (highest index != n among the row modes) has 16 | I_f
       int f = -1;
       for (int m = 0; m < N_ - 1; ++m)
@@ -480,6 +511,7 @@ class CpEngine {
       const char* slow = std::getenv("NTFG_TC_SLOW_GATHER");  // tests: force the per-row gather path
       if (slow && slow[0] == '1') p.gfast = 0;
     }
+    p.lay = tc_layout(ns, p.N, nmm, p.gfast != 0);
     p.partA = reinterpret_cast<float*>(partA_);
     p.partB = partB_;
     const int cols = ns * p.mtw * p.N;  // segment accumulators, then the running sums

@@ -86,7 +86,7 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   __shared__ uint64_t h_full[2], h_empty[2], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ double gs[2][64];
+  __shared__ __align__(16) double gs[2][64];
   __shared__ double red[kRcEpiWarps];
 
   const int tid = threadIdx.x, lane = tid & 31;
@@ -101,10 +101,10 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
 
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&h_full[b], kRcProdWarps * 32);
+      tc::mbar_init(&h_full[b], kRcProdWarps);  // one arrival per warp
       tc::mbar_init(&h_empty[b], 1);
       tc::mbar_init(&acc_full[b], 1);
-      tc::mbar_init(&acc_empty[b], kRcEpiWarps * 32);
+      tc::mbar_init(&acc_empty[b], kRcEpiWarps);
     }
   }
   tc::fence_barrier_init();
@@ -184,27 +184,63 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
         gs[st][pt] = g;
       }
       named_sync(2, kRcProdWarps * 32);
-      const double* fr = p.fac[f] + p.g.coord(row0, f) * R + pt;
       const uint32_t hhi = hbase + st * 2u * plane, hlo = hhi + plane;
-      int row = pt / R, r = pt - row * R;
+      if ((R & 3) == 0) {
+        // four consecutive ranks of one row per item: 32-byte loads (a warp
+        // reads 1 KB contiguous), one 16-byte store per plane (conflict-free
+        // with the 144-byte core-matrix stride), one address per four values
+        const int R4 = R >> 2;
+        const int kstep = PT % R4, rowstep4 = PT / R4, nchunk = kRcRows * R4;
+        const double2* fr = reinterpret_cast<const double2*>(p.fac[f] + p.g.coord(row0, f) * R);
+        int row = pt / R4, kc = pt - row * R4;
+#pragma unroll 4
+        for (int c = pt; c < nchunk; c += PT) {
+          const double2 v01 = __ldg(fr + 2 * c), v23 = __ldg(fr + 2 * c + 1);
+          double v[4] = {v01.x, v01.y, v23.x, v23.y};
+          if (npre >= 2) {
+            const double2 g01 = *reinterpret_cast<const double2*>(&gs[st][4 * kc]);
+            const double2 g23 = *reinterpret_cast<const double2*>(&gs[st][4 * kc + 2]);
+            v[0] *= g01.x; v[1] *= g01.y; v[2] *= g23.x; v[3] *= g23.y;
+          }
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float h = float(v[e]);
+            hi[e] = tf32_rna(h);
+            lo[e] = tf32_rna(h - __uint_as_float(hi[e]));
+          }
+          const uint32_t off = uint32_t(row >> 3) * sbo + uint32_t(kc) * kRcLbo + uint32_t(row & 7) * 16u;
+          tc::sts_v4(hhi + off, make_uint4(hi[0], hi[1], hi[2], hi[3]));
+          tc::sts_v4(hlo + off, make_uint4(lo[0], lo[1], lo[2], lo[3]));
+          kc += kstep;
+          row += rowstep4;
+          if (kc >= R4) {
+            kc -= R4;
+            ++row;
+          }
+        }
+      } else {
+        const double* fr = p.fac[f] + p.g.coord(row0, f) * R + pt;
+        int row = pt / R, r = pt - row * R;
 #pragma unroll 8
-      for (int e = pt; e < nel; e += PT) {
-        const double v = fr[e - pt];
-        const float h = float(npre >= 2 ? gs[st][r] * v : v);
-        const uint32_t hi = tf32_rna(h);
-        const uint32_t lo = tf32_rna(h - __uint_as_float(hi));
-        const uint32_t off = uint32_t(row >> 3) * sbo + uint32_t(r >> 2) * kRcLbo + uint32_t(row & 7) * 16u + uint32_t(r & 3) * 4u;
-        sts_b32(hhi + off, hi);
-        sts_b32(hlo + off, lo);
-        r += rstep;
-        row += rowstep;
-        if (r >= R) {
-          r -= R;
-          ++row;
+        for (int e = pt; e < nel; e += PT) {
+          const double v = fr[e - pt];
+          const float h = float(npre >= 2 ? gs[st][r] * v : v);
+          const uint32_t hi = tf32_rna(h);
+          const uint32_t lo = tf32_rna(h - __uint_as_float(hi));
+          const uint32_t off = uint32_t(row >> 3) * sbo + uint32_t(r >> 2) * kRcLbo + uint32_t(row & 7) * 16u + uint32_t(r & 3) * 4u;
+          sts_b32(hhi + off, hi);
+          sts_b32(hlo + off, lo);
+          r += rstep;
+          row += rowstep;
+          if (r >= R) {
+            r -= R;
+            ++row;
+          }
         }
       }
       tc::fence_proxy_async();
-      tc::arrive(&h_full[st]);
+      tc::warp_arrive(&h_full[st], lane);
     }
   } else {
     // ================= epilogue =================
@@ -244,7 +280,7 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
         tc::tmem_ld_wait();
         if (half == 1) {  // accumulator read: the MMAs of tile i + 2 may overwrite it
           tc::fence_before_sync();
-          tc::arrive(&acc_empty[st]);
+          tc::warp_arrive(&acc_empty[st], lane);
         }
 #pragma unroll
         for (int sub = 0; sub < 2; ++sub) {

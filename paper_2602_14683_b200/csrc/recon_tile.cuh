@@ -42,18 +42,26 @@ struct RtSmem {
 // constant factor back in per tile (exact: a power of two or 1).  NaN/Inf
 // models reach the tile sum through y itself, except at beta = 0 whose
 // clamp is the NaN-propagating select of tc_weights.
+// 1 / c for c >= eps (a normal fp32): the bare SFU reciprocal; __fdividef's
+// range scaling (five more instructions per entry) is for denormal divisors
+__device__ __forceinline__ float rcp_ftz(float c) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(c));
+  return r;
+}
+
 template <int BK>
 __device__ __forceinline__ void rt_weights(float x, float y, const TailConst& k, float& pv, float& qv, float& tacc) {
   if constexpr (BK == kBeta1) {
     const float c = fmaxf(y, k.e);
-    pv = __fdividef(x, c);
+    pv = x * rcp_ftz(c);
     qv = 1.f;
     tacc += (x > 0.f ? x * __logf(pv) : 0.f) - x + y;
-  } else if constexpr (BK == kBetaHalf) {  // t = 2 q (x + y)
+  } else if constexpr (BK == kBetaHalf) {  // q = c^-1/2, p = x c^-3/2 = x q^3; t = 2 q (x + y)
     const float c = fmaxf(y, k.e);
     const float rs = rsqrt_ftz(c);
     qv = rs;
-    pv = x * __fdividef(rs, c);
+    pv = (x * rs) * (rs * rs);
     tacc = fmaf(qv, x + y, tacc);
   } else if constexpr (BK == kBeta3Half) {
     const float c = fmaxf(y, k.e);
@@ -63,7 +71,7 @@ __device__ __forceinline__ void rt_weights(float x, float y, const TailConst& k,
     tacc = fmaf(qv, y * (2.f / 3.f) - 2.f * x, tacc);
   } else if constexpr (BK == kBeta0) {
     const float c = y < k.e ? k.e : y;
-    const float ic = __fdividef(1.f, c);
+    const float ic = rcp_ftz(c);
     qv = ic;
     pv = x * ic * ic;
     const float r = x * qv;
@@ -96,6 +104,17 @@ __device__ __forceinline__ void rt_split_pair(float a, float b, uint32_t& hi, ui
     hi = hu;
     lo = lu;
   }
+}
+
+// the same split without the tie test: `tie` collects (hi + lo as bf16) ^ hi so
+// that a block of entries is tested with ONE branch; a block with a tie is
+// redone with rt_split_pair (rare: ~2^-8 per entry)
+__device__ __forceinline__ void rt_split_pair_nocheck(float a, float b, uint32_t& hi, uint32_t& lo, uint32_t& tie) {
+  hi = bf16x2_bits(__floats2bfloat162_rn(a, b));
+  lo = bf16x2_bits(__floats2bfloat162_rn(a - bf16_lo_f(hi), b - bf16_hi_f(hi)));
+  const __nv_bfloat162 s2 = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&hi),
+                                    *reinterpret_cast<const __nv_bfloat162*>(&lo));
+  tie |= bf16x2_bits(s2) ^ hi;
 }
 
 // NPRE: number of row (prefix) modes when 1..3 and the fastest one has 32 | I

@@ -32,6 +32,13 @@ __device__ __forceinline__ void expect_tx(uint64_t* bar, unsigned bytes) {
 __device__ __forceinline__ void arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(bar)) : "memory");
 }
+// one arrival for the whole warp: every lane's prior accesses are ordered
+// before lane 0's (releasing) arrive by the warp barrier.  128 single-thread
+// arrivals per stage serialise on the barrier word; one per warp does not.
+__device__ __forceinline__ void warp_arrive(uint64_t* bar, int lane) {
+  __syncwarp();
+  if (lane == 0) arrive(bar);
+}
 __device__ __forceinline__ void wait(uint64_t* bar, unsigned phase) {
   asm volatile(
       "{\n"

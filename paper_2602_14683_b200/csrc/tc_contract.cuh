@@ -47,7 +47,12 @@ constexpr int kTcMaxTiles = 8;   // accumulator tiles per work item: ns * mtw
 // limit at N <= 32 (C2 K3 0.198 -> 0.189 ms); at N = 64 a second issuer gains
 // nothing and its registers push the kernel into spills, so it stays at one
 template <int N> __host__ __device__ constexpr int tc_issuers() { return N <= 32 ? 2 : 1; }
-template <int N> __host__ __device__ constexpr int tc_threads() { return 352 + 32 * (tc_issuers<N>() - 1); }
+// B-producer warps: one (stream, k-group, rank) item per thread per stage at
+// N = 64 (256 items).  A single warp per scheduler runs the ~300-instruction
+// stage body at ~0.2 IPC (1300 of the 1456 cycles a C5 stage may take at HBM
+// speed); two warps per scheduler hide each other's latencies.
+template <int N> __host__ __device__ constexpr int tc_bwarps() { return N > 32 ? 8 : 4; }
+template <int N> __host__ __device__ constexpr int tc_threads() { return 32 * (tc_bwarps<N>() + 7 + (tc_issuers<N>() - 1)); }
 constexpr int kTcBSbo = 272;    // bytes between 8-column groups of a B tile (256 + 16: bank spread)
 constexpr int kTcGModes = 3;    // factor modes gathered through the cp.async ring (more: direct fp64)
 constexpr size_t kTcSmemMax = 227 * 1024 - 5120;  // dynamic budget (static smem 4.3 KB + 1 KB alignment slack)
@@ -58,6 +63,7 @@ struct TcLayout {
   uint32_t b_tile;             // bytes of one bf16 B tile
   uint32_t b_off, ring_off;    // region offsets
   int nst, gdepth, gmodes;     // stages, gather ring depth, gathered modes
+  uint32_t g_stream, g_slot;   // bytes of one stream's gather regions / one gather slot (all streams)
 
   uint32_t total;
 };
@@ -128,25 +134,29 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   const int64_t K = p.g.K;
   const int64_t In = p.g.dims[p.n];
   constexpr int N = NMAX;  // UMMA N (host launches the instance matching the rank)
+  // warp roles: [0, kB) B producers, kB..kB+3 epilogue (TMEM lane quarter = warp % 4),
+  // then TMA producer, MMA issuer (+ TMEM allocator), gather warp, second issuer
+  constexpr int kB = tc_bwarps<NMAX>();
+  constexpr int kWTma = kB + 4, kWMma = kB + 5, kWGather = kB + 6, kWMma2 = kB + 7;
 
   if (tid == 0) {
     for (int s = 0; s < L.nst; ++s) {
       tc::mbar_init(&a_full[s], 1);
-      tc::mbar_init(&b_full[s], 128);
+      tc::mbar_init(&b_full[s], kB);    // one arrival per B-producer warp
       tc::mbar_init(&empty[s], tc_issuers<NMAX>());
     }
     for (int g = 0; g < L.gdepth; ++g) {
       tc::mbar_init(&g_full[g], 1);
-      tc::mbar_init(&g_empty[g], 128);
+      tc::mbar_init(&g_empty[g], kB);
     }
     for (int t = 0; t < kTcMaxTiles; ++t) {
       tc::mbar_init(&acc_full[t], 1);     // committed by the tile's issuer
-      tc::mbar_init(&acc_empty[t], 128);  // drained by the epilogue threads
+      tc::mbar_init(&acc_empty[t], 4);  // drained by the epilogue warps
     }
   }
   tc::fence_barrier_init();
-  if (warp == 9) tc::tmem_alloc(&tmem_base, uint32_t(p.tmem_cols));
-  if (warp == 8 && lane == 0)
+  if (warp == kWMma) tc::tmem_alloc(&tmem_base, uint32_t(p.tmem_cols));
+  if (warp == kWTma && lane == 0)
     for (int s = 0; s < p.ns; ++s) {
       tc::prefetch_map(&maps.m[s][0]);
       tc::prefetch_map(&maps.m[s][1]);
@@ -183,7 +193,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     return smem + L.b_off + ((size_t(slot) * 2 + s) * 2 + plane) * L.b_tile;
   };
 
-  if (warp == 8) {
+  if (warp == kWTma) {
     // ================= TMA producer =================
     // converged warp, one elected lane issues (uniform operands: no per-lane
     // operand marshalling around the TMA instructions)
@@ -226,9 +236,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 6] = clock64() - t00;
       }
     }
-  } else if (warp == 9 || (warp == 11 && tc_issuers<NMAX>() > 1)) {
+  } else if (warp == kWMma || (warp == kWMma2 && tc_issuers<NMAX>() > 1)) {
     // ================= MMA issuers =================
-    // issuer i (warp 9: 0, warp 11: 1) owns the accumulator tiles t = s * mtw + m
+    // issuer i (first MMA warp: 0, second: 1) owns the accumulator tiles t = s * mtw + m
     // with t % 2 == i.  The accumulator of a tile restarts from zero every
     // p.seg stages (a "segment"); the epilogue adds each finished segment into
     // running sums (a second TMEM region) on the CUDA cores: long fp32
@@ -244,7 +254,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     // makes the compiler wrap every tcgen05.mma in an elect/R2UR loop, which
     // cost ~150 cycles per MMA against the 43 + N/2 the tensor pipe needs
     // (tools/mma_probe.cu).
-    const int issuer = warp == 9 ? 0 : 1;
+    const int issuer = warp == kWMma ? 0 : 1;
     const uint32_t idesc = tc::idesc_bf16_f32(128, N, true, false);
     const int ntile = p.ns * p.mtw;
     const uint64_t a_desc0 = tc::desc_mn_sw128(smem, 2048, 1024);
@@ -298,7 +308,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         }
       }
     }
-  } else if (warp == 10) {
+  } else if (warp == kWGather) {
     // ================= factor-row gathers (bulk async copies) =================
     // gather slot q % gdepth holds, per stream, gm regions of [16][N] floats.
     // Fast path (p.gfast: the fastest off-mode f has 16 | I_f, so a stage's 16
@@ -319,16 +329,16 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     const unsigned bytes = p.gfast ? unsigned(p.ns) * (regb + unsigned(gm - 1) * rowb)
                                    : unsigned(16 * gm * p.ns) * rowb;
     unsigned char* ring = smem + L.ring_off;
-    uint32_t q = 0;
+    int gs = 0;
+    uint32_t gph = 1;  // producer parity: the first pass finds every gather slot free
     unsigned long long gw = 0, g00 = p.trace ? clock64() : 0;
     if (gm > 0 && !(p.ablate & 1)) {
       for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
         int64_t j0, j1, itgt, split;
         unit_range(w / p.G, j0, j1, itgt, split);
-        for (int64_t jb = j0; jb < j1; jb += kTcRows, ++q) {
-          const int gs = int(q % unsigned(L.gdepth));
+        for (int64_t jb = j0; jb < j1; jb += kTcRows) {
           const unsigned long long tq = p.trace ? clock64() : 0;
-          tc::wait(&g_empty[gs], ((q / unsigned(L.gdepth)) & 1u) ^ 1u);
+          tc::wait(&g_empty[gs], gph);
           if (p.trace) gw += clock64() - tq;
           if (lane == 0) tc::expect_tx(&g_full[gs], bytes);
           __syncwarp();
@@ -336,7 +346,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
             if (lane < gm * p.ns) {
               const int mi = lane % gm, st = lane / gm;
               const int64_t row = row_of(jb, itgt);
-              unsigned char* dst = ring + (size_t(gs * p.ns + st) * gm + mi) * regb;
+              // compact fast-path slot: [16][N] rows of the fastest off-mode, then one row per other mode
+              unsigned char* dst = ring + size_t(gs) * L.g_slot + size_t(st) * L.g_stream +
+                                   (mi == 0 ? 0u : regb + unsigned(mi - 1) * rowb);
               if (mi == 0)
                 tma::bulk_g2s(dst, p.fac32[st][fm] + p.g.coord(row, fm) * N, regb, &g_full[gs]);
               else
@@ -347,9 +359,13 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
               const int kk = c & 15, mi = (c >> 4) % gm, st = (c >> 4) / gm;
               const int64_t j = jb + kk < j1 ? jb + kk : j1 - 1;
               const int64_t crd = p.g.coord(row_of(j, itgt), mm[mi]);
-              unsigned char* dst = ring + ((size_t(gs * p.ns + st) * gm + mi) * 16 + kk) * rowb;
+              unsigned char* dst = ring + size_t(gs) * L.g_slot + size_t(st) * L.g_stream + (size_t(mi) * 16 + kk) * rowb;
               tma::bulk_g2s(dst, p.fac32[st][mm[mi]] + crd * N, rowb, &g_full[gs]);
             }
+          }
+          if (++gs == L.gdepth) {
+            gs = 0;
+            gph ^= 1u;
           }
         }
       }
@@ -358,7 +374,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 3] = gw;
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 4] = clock64() - g00;
     }
-  } else if (warp < 4) {
+  } else if (warp < kB) {
     // ================= B-tile (M rows) producers =================
     // work item = (stream s, k group kg of 8 stage rows, rank column r): the
     // 8 products M(8kg..8kg+7, r) are one 16-byte core-matrix row of the
@@ -374,45 +390,49 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     const uint32_t ring = tc::saddr(smem + L.ring_off);
     const uint32_t btiles = tc::saddr(smem + L.b_off);
     const int nitems = p.ns * 2 * N;
-    constexpr int kMaxItems = 2;  // ns * 2 * N <= 256
-    uint32_t q = 0;
+    constexpr int kBT = kB * 32;                                  // B-producer threads
+    constexpr int kMaxItems = (4 * N + kBT - 1) / kBT;            // ns * 2 * N items per stage
+    int slot = -1, gs = -1;           // ring positions (advanced at the top of every stage)
+    uint32_t sph = 0, gph = 1;        // sph: parity the slot's "empty" wait uses (ph ^ 1 trick); gph: gather "full" parity
     unsigned long long bw0 = 0, bw1 = 0, b00 = p.trace ? clock64() : 0;
     for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
       int64_t j0, j1, itgt, split;
       unit_range(w / p.G, j0, j1, itgt, split);
-      for (int64_t jb = j0; jb < j1; jb += kTcRows, ++q) {
-        const int slot = int(q % unsigned(L.nst));
+      for (int64_t jb = j0; jb < j1; jb += kTcRows) {
+        if (++slot == L.nst) slot = 0;
+        if (slot == 0) sph ^= 1u;    // first pass: 1 (slots start free)
+        if (++gs == L.gdepth) gs = 0;
+        if (gs == 0) gph ^= 1u;      // first pass: 0
         if (p.ablate & 1) {
-          tc::wait(&empty[slot], ((q / unsigned(L.nst)) & 1u) ^ 1u);
-          tc::arrive(&b_full[slot]);
+          tc::wait(&empty[slot], sph);
+          tc::warp_arrive(&b_full[slot], lane);
           continue;
         }
-        const int gs = int(q % unsigned(L.gdepth));
         const int nvalid = int(j1 - jb < kTcRows ? j1 - jb : kTcRows);
         unsigned long long tq = p.trace ? clock64() : 0;
-        if (gm > 0) tc::wait(&g_full[gs], (q / unsigned(L.gdepth)) & 1u);
+        if (gm > 0) tc::wait(&g_full[gs], gph);
         if (p.trace) { bw0 += clock64() - tq; }
         uint4 hv[kMaxItems], lv[kMaxItems];
 #pragma unroll
         for (int it = 0; it < kMaxItems; ++it) {
-          const int i = tid + it * 128;
+          const int i = tid + it * kBT;
           if (i >= nitems) break;
           const int r = i % N, kg = (i / N) & 1, st = i / (2 * N);
           float v[8];
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) v[kk] = kg * 8 + kk < nvalid ? 1.f : 0.f;
-          const uint32_t reg0 = ring + uint32_t((gs * p.ns + st) * gm) * 16u * uint32_t(N * 4) + uint32_t(r) * 4;
+          for (int kk = 0; kk < 8; ++kk) v[kk] = 1.f;
+          const uint32_t reg0 = ring + uint32_t(gs) * L.g_slot + uint32_t(st) * L.g_stream + uint32_t(r) * 4;
           if (p.gfast && gm > 0) {  // v = (prod of the other modes' rows, ascending) * A_f rows
             float g = 1.f;
             for (int mi = 1; mi < gm; ++mi) {
-              const float f = tc::lds_f32(reg0 + uint32_t(mi) * 16u * uint32_t(N * 4));
+              const float f = tc::lds_f32(reg0 + 16u * uint32_t(N * 4) + uint32_t(mi - 1) * uint32_t(N * 4));
               g = mi == 1 ? f : g * f;
             }
             const uint32_t base = reg0 + uint32_t(kg * 8) * uint32_t(N * 4);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const float f = tc::lds_f32(base + uint32_t(kk) * uint32_t(N * 4));
-              v[kk] *= gm > 1 ? g * f : f;
+              v[kk] = gm > 1 ? g * f : f;
             }
           } else {
             for (int mi = 0; mi < gm; ++mi) {
@@ -430,19 +450,24 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
                 v[kk] = r < p.R ? float(double(v[kk]) * p.mfac[st][mm[c2]][p.g.coord(row, mm[c2]) * p.R + r]) : 0.f;
             }
           }
+          if (nvalid < kTcRows) {  // last stage of a unit: rows past its end contribute nothing
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              if (kg * 8 + kk >= nvalid) v[kk] = 0.f;
+          }
           uint32_t h[4], l[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) bf16_split_pair_fast(v[2 * e], v[2 * e + 1], h[e], l[e]);
           hv[it] = make_uint4(h[0], h[1], h[2], h[3]);
           lv[it] = make_uint4(l[0], l[1], l[2], l[3]);
         }
-        if (gm > 0) tc::arrive(&g_empty[gs]);
+        if (gm > 0) tc::warp_arrive(&g_empty[gs], lane);
         tq = p.trace ? clock64() : 0;
-        tc::wait(&empty[slot], ((q / unsigned(L.nst)) & 1u) ^ 1u);
+        tc::wait(&empty[slot], sph);
         if (p.trace) { bw1 += clock64() - tq; }
 #pragma unroll
         for (int it = 0; it < kMaxItems; ++it) {
-          const int i = tid + it * 128;
+          const int i = tid + it * kBT;
           if (i >= nitems) break;
           const int r = i % N, kg = (i / N) & 1, st = i / (2 * N);
           const uint32_t off = uint32_t(r / 8) * kTcBSbo + uint32_t(kg) * 128 + uint32_t(r % 8) * 16;
@@ -451,7 +476,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
           tc::sts_v4(tile + L.b_tile + off, lv[it]);
         }
         tc::fence_proxy_async();
-        tc::arrive(&b_full[slot]);
+        tc::warp_arrive(&b_full[slot], lane);
       }
     }
     if (p.trace && tid == 0) {
@@ -468,7 +493,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     // case B dots G with the last-mode factor over k: out(r) = sum_k
     // F_last(k, r) G(k, r) (fp64 across k, m-tiles and units).
     const int quarter = warp & 3;
-    const int et = tid - 128;  // 0..127
+    const int et = tid - kB * 32;  // 0..127
     const int ntile = p.ns * p.mtw;
     const uint32_t lanes = uint32_t(quarter * 32) << 16;
     const uint32_t run = tmem + lanes + uint32_t(cols_per_buf);
@@ -499,7 +524,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
             }
           }
           tc::fence_before_sync();
-          tc::arrive(&acc_empty[t]);  // the segment tile is read: its next segment may start
+          tc::warp_arrive(&acc_empty[t], lane);  // the segment tile is read: its next segment may start
         }
         tc::tmem_st_wait();
       }
@@ -577,7 +602,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 9) tc::tmem_dealloc(tmem, uint32_t(p.tmem_cols));
+  if (warp == kWMma) tc::tmem_dealloc(tmem, uint32_t(p.tmem_cols));
 }
 
 #endif  // NTFG_TC_CONTRACT_IMPL
