@@ -284,3 +284,35 @@ def mu_unfold_cp_sweep(x, factors, beta, eps=1e-12):
     _check(lib().ntfref_mu_unfold_cp_sweep(C.c_int(x.ndim), _u64(x.shape).ctypes.data_as(_U), _d(x), C.c_int(rank),
                                            _d(f), C.c_double(beta), C.c_double(eps)))
     return _split(f, [np.shape(a) for a in factors])
+
+
+def joint_surrogate_cp(theta, ref, x, beta, eps=1e-12):
+    """reference oracle::eval_joint_surrogate_cp (oracle.cpp:215-243)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    rank = ref[0].shape[1]
+    out = C.c_double(0)
+    _check(lib().ntfref_joint_surrogate_cp(C.c_int(x.ndim), _u64(x.shape).ctypes.data_as(_U), _d(x), C.c_int(rank),
+                                           _d(_cat(theta)), _d(_cat(ref)), C.c_double(beta), C.c_double(eps),
+                                           C.byref(out)))
+    return out.value
+
+
+def joint_surrogate_tucker(theta, ref, x, beta, eps=1e-12):
+    """reference oracle::eval_joint_surrogate_tucker (oracle.cpp:245-281); models are (core, factors)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    tc = np.ascontiguousarray(theta[0], dtype=np.float64)
+    rc = np.ascontiguousarray(ref[0], dtype=np.float64)
+    out = C.c_double(0)
+    _check(lib().ntfref_joint_surrogate_tucker(C.c_int(x.ndim), _u64(x.shape).ctypes.data_as(_U), _d(x),
+                                               _u64(rc.shape).ctypes.data_as(_U), _d(tc), _d(_cat(theta[1])),
+                                               _d(rc), _d(_cat(ref[1])), C.c_double(beta), C.c_double(eps),
+                                               C.byref(out)))
+    return out.value
+
+
+def scalar_minimizer(num, den, beta, floor=1e-12):
+    """reference oracle::scalar_minimizer and jmm_scalar_objective at the minimizer (oracle.cpp:285-302)."""
+    u, g = C.c_double(0), C.c_double(0)
+    _check(lib().ntfref_scalar_minimizer(C.c_double(num), C.c_double(den), C.c_double(beta), C.c_double(floor),
+                                         C.byref(u), C.byref(g)))
+    return u.value, g.value

@@ -25,6 +25,7 @@
 #include "ntf/divergence.hpp"
 #include "ntf/errors.hpp"
 #include "ntf/io.hpp"
+#include "ntf/oracle.hpp"
 #include "ntf/tensor.hpp"
 #include "ntf/tucker.hpp"
 #include "ntf/unfold.hpp"
@@ -482,5 +483,38 @@ SHIM int ntfref_write_trace(const char* path, int n, const double* times, const 
         std::vector<ntf::TraceRecord> r(static_cast<std::size_t>(n));
         for (int i = 0; i < n; ++i) r[std::size_t(i)] = ntf::TraceRecord{std::size_t(i), times[i], losses[i]};
         ntf::write_trace(path, r);
+    });
+}
+
+// ---- joint-surrogate oracle (reference oracle.hpp:41-80, oracle.cpp:181-281) -------
+
+SHIM int ntfref_joint_surrogate_cp(int order, const std::uint64_t* dims, const double* x, int rank,
+                                   const double* theta, const double* ref, double beta, double eps,
+                                   double* out) {
+    return guarded([&] {
+        const auto shape = to_shape(order, dims);
+        *out = ntf::oracle::eval_joint_surrogate_cp(cp_in(shape, rank, theta), cp_in(shape, rank, ref),
+                                                    tensor_in(shape, x), ntf::BetaParam(beta), eps);
+    });
+}
+
+SHIM int ntfref_joint_surrogate_tucker(int order, const std::uint64_t* dims, const double* x,
+                                       const std::uint64_t* ranks, const double* theta_core,
+                                       const double* theta, const double* ref_core, const double* ref,
+                                       double beta, double eps, double* out) {
+    return guarded([&] {
+        const auto shape = to_shape(order, dims);
+        const auto rk = to_shape(order, ranks);
+        *out = ntf::oracle::eval_joint_surrogate_tucker(tucker_in(shape, rk, theta_core, theta),
+                                                        tucker_in(shape, rk, ref_core, ref),
+                                                        tensor_in(shape, x), ntf::BetaParam(beta), eps);
+    });
+}
+
+SHIM int ntfref_scalar_minimizer(double num, double den, double beta, double floor, double* u, double* g) {
+    return guarded([&] {
+        const ntf::BetaParam p(beta);
+        *u = ntf::oracle::scalar_minimizer(num, den, p, floor);
+        *g = ntf::oracle::jmm_scalar_objective(*u, num, den, p);
     });
 }

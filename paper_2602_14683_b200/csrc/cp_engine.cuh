@@ -109,8 +109,10 @@ class CpEngine {
   // x-only objective constant for the tensor-core recon (see xconst_kernel);
   // computed when the data arrives, outside any captured graph.
   bool split_objective() const { return tc_ && (bk_ == kBetaHalf || bk_ == kBeta3Half || bk_ == kBetaGeneric); }
+  // the tile / tcgen05 reconstructions evaluate the model part of d_beta only
+  bool rt_objective() const { return bk_ == kBetaHalf || bk_ == kBeta3Half || bk_ == kBetaGeneric; }
   void compute_xconst() {
-    if (!split_objective()) return;
+    if (!(split_objective() || (rt_objective() && (recon_tc_ok(true) || recon_tc_ok(false))))) return;
     if (!xconst_) xconst_ = c_.buf<double>("cp.xconst", 1 + kXconstGrid);
     xconst_kernel<T><<<kXconstGrid, 256, 0, c_.stream>>>(x_, E_, beta_, xconst_ + 1);
     NTFG_LAUNCHED(c_);
@@ -248,8 +250,11 @@ class CpEngine {
     // planes pass and for objective-only passes
     const bool tile = tc_ && sizeof(T) == 4 && !htab && !xhout && !pout && !qout && rows_tma_ok(x_) &&
                       g_.K % kRtCols == 0 && RP_ <= 64 && !tile_disabled();
-    obj_split_ = tile ? split_objective() : (planes_out_ && split_objective());
-    if (tile && recon_tc_ok()) {
+    // tcgen05 reconstruction: also with fp32 P/Q outputs and with a row table
+    const bool rtc = sizeof(T) == 4 && !xhout && rows_tma_ok(x_) && RP_ <= 64 && !tile_disabled() &&
+                     recon_tc_ok(htab != nullptr) && (tile || htab || pout || !tc_);
+    obj_split_ = (tile || rtc) ? rt_objective() : (planes_out_ && split_objective());
+    if (rtc) {
       // Xhat on the tensor cores (recon_tc.cuh): one persistent CTA per SM,
       // grid a multiple of the k tiles
       p.ktiles = int(g_.K / kRcCols);
@@ -1209,10 +1214,10 @@ class CpEngine {
 
   // tcgen05 reconstruction: the fastest row mode has 128 | I (a 128-row tile
   // then shares the slower coordinates), K = 128..512 in 128 steps
-  bool recon_tc_ok() const {
+  bool recon_tc_ok(bool row_table = false) const {
     static const bool off = [] { const char* e = std::getenv("NTFG_DISABLE_RECON_TC"); return e && e[0] == '1'; }();
-    return !off && N_ >= 2 && g_.dims[N_ - 2] % kRcRows == 0 && g_.small_rows && g_.K % kRcCols == 0 &&
-           g_.K / kRcCols <= 4;
+    if (off || sizeof(T) != 4 || N_ < 2 || !g_.small_rows || g_.K % kRcCols != 0 || g_.K / kRcCols > 4) return false;
+    return row_table ? g_.rows % kRcRows == 0 : g_.dims[N_ - 2] % kRcRows == 0;
   }
   static bool tile_disabled() {  // perf experiments: NTFG_DISABLE_RTILE=1 keeps recon3
     static const bool v = [] { const char* e = std::getenv("NTFG_DISABLE_RTILE"); return e && e[0] == '1'; }();

@@ -31,7 +31,10 @@
 // Eligible when the fastest row mode has 128 | I (a tile's rows then share the
 // slower coordinates and run over 128 consecutive rows of that factor: one
 // contiguous block) and K is a multiple of 128 up to 512; everything else
-// stays on recon_tile_kernel.
+// stays on recon_tile_kernel.  With a row table (p.htab, the Tucker partial
+// chain Y(row, j), tensor.cpp:408-419) H is that table and 128 | rows suffices.
+// Outputs: bf16 hi/lo planes (tensor-core K3), fp32 P/Q arrays (CUDA-core
+// contraction paths and the Tucker engine), or the objective only.
 #pragma once
 #include "recon_tile.cuh"
 #include "tc_common.cuh"
@@ -168,8 +171,8 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
     // ================= H producers =================
     constexpr int PT = kRcProdWarps * 32;
     const int pt = tid - kRcEpiWarps * 32;  // 0..PT-1
-    const int npre = p.g.order - 1;
-    const int f = npre - 1;  // fastest row mode
+    const int npre = p.htab ? 1 : p.g.order - 1;  // row table: H is read as is
+    const int f = p.g.order - 2;                    // fastest row mode
     const int rstep = PT % R, rowstep = PT / R;
     const int nel = kRcRows * R;
     const uint32_t hbase = tc::saddr(smem) + 2u * plane;
@@ -184,6 +187,9 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
         gs[st][pt] = g;
       }
       named_sync(2, kRcProdWarps * 32);
+      // H rows of the tile: 128 consecutive rows of the fastest row mode's
+      // factor, or (Tucker partial chain) of the row table itself
+      const double* hsrc = p.htab ? p.htab + row0 * R : p.fac[f] + p.g.coord(row0, f) * R;
       const uint32_t hhi = hbase + st * 2u * plane, hlo = hhi + plane;
       if ((R & 3) == 0) {
         // four consecutive ranks of one row per item: 32-byte loads (a warp
@@ -191,7 +197,7 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
         // with the 144-byte core-matrix stride), one address per four values
         const int R4 = R >> 2;
         const int kstep = PT % R4, rowstep4 = PT / R4, nchunk = kRcRows * R4;
-        const double2* fr = reinterpret_cast<const double2*>(p.fac[f] + p.g.coord(row0, f) * R);
+        const double2* fr = reinterpret_cast<const double2*>(hsrc);
         int row = pt / R4, kc = pt - row * R4;
 #pragma unroll 4
         for (int c = pt; c < nchunk; c += PT) {
@@ -220,7 +226,7 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
           }
         }
       } else {
-        const double* fr = p.fac[f] + p.g.coord(row0, f) * R + pt;
+        const double* fr = hsrc + pt;
         int row = pt / R, r = pt - row * R;
 #pragma unroll 8
         for (int e = pt; e < nel; e += PT) {
@@ -254,6 +260,8 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
     const float oscale = rt_obj_scale<BK>(tk);
     const bool want_obj = p.obj != nullptr;
     const bool store = p.planes[0] != nullptr;
+    float* const pout32 = p.pout;
+    float* const qout32 = p.qout;
     unsigned short* const pl0 = static_cast<unsigned short*>(p.planes[0]);
     unsigned short* const pl1 = static_cast<unsigned short*>(p.planes[1]);
     unsigned short* const pl2 = static_cast<unsigned short*>(p.planes[2]);
@@ -293,6 +301,14 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
             rt_weights<BK>(x, y, tk, pw[jj], qw[jj], tacc);
             ymin = fminf(ymin, y);
             xmin = fminf(xmin, x);
+          }
+          if (pout32) {  // fp32 P/Q arrays (CUDA-core contraction paths, Tucker): 128-byte rows per warp
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const int64_t o = ob + (j0 + jj) * K;
+              pout32[o] = pw[jj];
+              if (qout32) qout32[o] = qw[jj];
+            }
           }
           if (store) {
 #pragma unroll

@@ -105,7 +105,13 @@ class TuckerEngine {
     const int64_t total = outer * na * inner;
     const int grid = int(std::min<int64_t>(ceil_div(total, 256), int64_t(c_.sm_count) * 16));
     const int ph = c_.prof_begin(2);
-    ttm_kernel<<<std::max(grid, 1), 256, 0, c_.stream>>>(in, outer, nb, inner, M, na, trans, out);
+    const int cgrid = int(std::min<int64_t>(outer * ceil_div(inner, 32), int64_t(c_.sm_count) * 8));
+    if (trans && nb >= 64 && (na == 8 || na == 16)) {  // contracting product: split-b tiles
+      if (na == 8) ttm_contract_kernel<8><<<cgrid, 256, 0, c_.stream>>>(in, outer, nb, inner, M, out);
+      else ttm_contract_kernel<16><<<cgrid, 256, 0, c_.stream>>>(in, outer, nb, inner, M, out);
+    } else {
+      ttm_kernel<<<std::max(grid, 1), 256, 0, c_.stream>>>(in, outer, nb, inner, M, na, trans, out);
+    }
     NTFG_LAUNCHED(c_);
     c_.prof_end(ph);
     shape[axis] = na;
@@ -132,14 +138,44 @@ class TuckerEngine {
     const int64_t warps_needed = rows_;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps_needed, 8), int64_t(c_.sm_count) * 8)));
     const int ph = c_.prof_begin(1);
-    switch (RP_) {
-      case 8: rowgemm_kernel<T, 8><<<grid, 256, 0, c_.stream>>>(S, rows_, I_[L_], stageS_, int(J_[L_]), T1_); break;
-      case 16: rowgemm_kernel<T, 16><<<grid, 256, 0, c_.stream>>>(S, rows_, I_[L_], stageS_, int(J_[L_]), T1_); break;
-      case 32: rowgemm_kernel<T, 32><<<grid, 256, 0, c_.stream>>>(S, rows_, I_[L_], stageS_, int(J_[L_]), T1_); break;
-      default: rowgemm_kernel<T, 64><<<grid, 256, 0, c_.stream>>>(S, rows_, I_[L_], stageS_, int(J_[L_]), T1_); break;
+    const int64_t K = I_[L_];
+    bool tiled = false;
+    if constexpr (sizeof(T) == 4) {
+      // tiled fp32 kernel: 32-column stages, 16-byte rows, F resident in shared memory
+      tiled = K % kRgCols == 0 && (reinterpret_cast<uintptr_t>(S) % 16) == 0 && size_t(K) * RP_ * 4 <= 64 * 1024;
+      if (tiled) {
+        const int tgrid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows_, kRgRows), int64_t(c_.sm_count) * 2)));
+        switch (RP_) {
+          case 8: launch_rg<8>(tgrid, S, K); break;
+          case 16: launch_rg<16>(tgrid, S, K); break;
+          case 32: launch_rg<32>(tgrid, S, K); break;
+          default: launch_rg<64>(tgrid, S, K); break;
+        }
+      }
+    }
+    if (!tiled) {
+      switch (RP_) {
+        case 8: rowgemm_kernel<T, 8><<<grid, 256, 0, c_.stream>>>(S, rows_, I_[L_], stageS_, int(J_[L_]), T1_); break;
+        case 16: rowgemm_kernel<T, 16><<<grid, 256, 0, c_.stream>>>(S, rows_, I_[L_], stageS_, int(J_[L_]), T1_); break;
+        case 32: rowgemm_kernel<T, 32><<<grid, 256, 0, c_.stream>>>(S, rows_, I_[L_], stageS_, int(J_[L_]), T1_); break;
+        default: rowgemm_kernel<T, 64><<<grid, 256, 0, c_.stream>>>(S, rows_, I_[L_], stageS_, int(J_[L_]), T1_); break;
+      }
     }
     NTFG_LAUNCHED(c_);
     c_.prof_end(ph);
+  }
+  template <int JP>
+  void launch_rg(int grid, const T* S, int64_t K) {
+    if constexpr (sizeof(T) == 4) {
+      const size_t sm = RgSmem<JP>::total(K);
+      static size_t attr = 0;
+      if (sm > attr) {
+        cuda_check(cudaFuncSetAttribute(rowgemm_tiled_kernel<JP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),
+                   "cudaFuncSetAttribute");
+        attr = sm;
+      }
+      rowgemm_tiled_kernel<JP><<<grid, 64 * (JP / 8), sm, c_.stream>>>(S, rows_, K, stageS_, int(J_[L_]), T1_);
+    }
   }
 
   // multimode contraction of S against all factors -> core-shaped out

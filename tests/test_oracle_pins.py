@@ -200,3 +200,72 @@ def test_coo_synthetic_conventions():
     assert idx.dtype == np.int32 and idx.min() >= 0 and idx[:, 1].max() < 50
     assert vals.min() == 1.0  # failures-count geometric: support {1, 2, ...}
     assert np.bincount(idx[:, 1]).argmax() == 0  # Zipf head at index 0
+
+
+# ---- joint-surrogate oracle (reference oracle.cpp:181-302, tests/test_oracle.cpp:44-160) ----
+
+def _surrogate_case(seed, dims=(5, 4, 3), rank=2):
+    rng = np.random.default_rng(seed)
+    x = 0.1 + rng.random(dims)
+    ref = [0.1 + rng.random((d, rank)) for d in dims]
+    theta = [a * (1.0 + 0.1 * rng.random(a.shape)) for a in ref]
+    return x, ref, theta
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 1.5])
+def test_joint_surrogate_tight_majorizes_and_descends(beta):
+    # test_oracle.cpp:44-70, 117-131: tight at the reference, majorizes the
+    # objective, nonincreasing across joint inner updates
+    x, ref, _ = _surrogate_case(2)
+    g = O.eval_joint_surrogate_cp(ref, ref, x, beta)
+    d = O.D_beta(x, O.cp_reconstruct(ref), beta)
+    assert abs(g - d) <= 1e-10 * (1.0 + d)
+    rng = np.random.default_rng(6)
+    for _ in range(20):
+        theta = [a * (1.0 + 0.1 * rng.random(a.shape)) for a in ref]
+        assert O.eval_joint_surrogate_cp(theta, ref, x, beta) >= O.D_beta(x, O.cp_reconstruct(theta), beta) - 1e-10 * (1 + d)
+    ctx = O.make_jcomm_reference(ref, x, beta, 1e-12)
+    cur, gprev = [a.copy() for a in ref], g
+    for _ in range(3):
+        for n in range(3):
+            cur = O.jcomm_inner_update(cur, ctx, n, beta, 1e-12)
+            nxt = O.eval_joint_surrogate_cp(cur, ref, x, beta)
+            assert nxt <= gprev + 1e-12 * (1.0 + abs(gprev))
+            gprev = nxt
+
+
+def test_joint_surrogate_single_component_and_scalar_minimizer_kats():
+    # test_oracle.cpp:72-81, 133-160
+    g = O.eval_joint_surrogate_cp([np.array([[2.0]]), np.array([[1.0]])], [np.ones((1, 1)), np.ones((1, 1))],
+                                  np.array([[2.0]]), 1.0)
+    assert abs(g - float(O.d_beta(2.0, 2.0, 1.0))) <= 1e-12
+    for beta in (0.0, 0.5, 1.0, 1.5):
+        assert O.scalar_minimizer(3.0, 3.0, beta, 1e-12) == 1.0
+        assert O.scalar_minimizer(0.0, 2.0, beta, 1e-9) == 1e-9
+        rng = np.random.default_rng(3)
+        for _ in range(10):
+            num, den = 0.05 + 3.0 * rng.random(), 0.05 + 3.0 * rng.random()
+            u = O.scalar_minimizer(num, den, beta, 1e-12)
+            gu = O.jmm_scalar_objective(u, num, den, beta)
+            for k in range(100):
+                cand = u * 10.0 ** (-2.0 + 4.0 * k / 99.0)
+                assert gu <= O.jmm_scalar_objective(cand, num, den, beta) + 1e-12 * (1.0 + abs(gu))
+    with pytest.raises(O.DomainError):
+        O.scalar_minimizer(1.0, 0.0, 0.5, 1e-12)
+
+
+@pytest.mark.skipif(not R.available(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 1.5])
+def test_joint_surrogate_matches_compiled_reference(beta):
+    x, ref, theta = _surrogate_case(11, dims=(4, 3, 2, 3), rank=3)
+    want = R.joint_surrogate_cp(theta, ref, x, beta)
+    assert abs(O.eval_joint_surrogate_cp(theta, ref, x, beta) - want) <= 1e-12 * (1.0 + abs(want))
+    assert abs(O.eval_joint_surrogate_cp(theta, ref, x, beta, slab=3) - want) <= 1e-12 * (1.0 + abs(want))
+    rng = np.random.default_rng(12)
+    tref = (0.1 + rng.random((2, 2, 2, 2)), [0.1 + rng.random((d, 2)) for d in x.shape])
+    tth = (tref[0] * 1.3, [a * 1.1 for a in tref[1]])
+    want = R.joint_surrogate_tucker(tth, tref, x, beta)
+    assert abs(O.eval_joint_surrogate_tucker(tth, tref, x, beta) - want) <= 1e-12 * (1.0 + abs(want))
+    u, gu = R.scalar_minimizer(1.7, 0.9, beta)
+    assert u == O.scalar_minimizer(1.7, 0.9, beta, 1e-12)
+    assert abs(gu - O.jmm_scalar_objective(u, 1.7, 0.9, beta)) <= 1e-14 * (1.0 + abs(gu))

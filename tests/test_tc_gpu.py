@@ -151,3 +151,26 @@ def test_recon_tc_data_floor_and_domain_flags():
     x[0, 5, 7] = 0.0
     with pytest.raises(ntf.NumericalError, match="data-floor"):
         ntf.jcomm_fit(x, f, ntf.FitConfig(beta=0.0, rank=4, max_iters=2, precision="f32"))
+
+
+# Large-scale inner-descent check of the fp32 tensor-core path with the
+# joint-surrogate oracle (reference oracle.cpp:215-243; acceptance criterion 4,
+# acceptance.cpp:176-200): G(theta | ref) is tight at the reference and does not
+# increase across the GPU's joint inner updates (fp32 tolerance).
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 1.5])
+def test_tc_inner_updates_descend_the_joint_surrogate(beta):
+    dims, rank = (24, 128, 128), 12
+    x, f = problem(dims, rank, 29)
+    x = x.astype(np.float32).astype(np.float64)
+    ctx = ntf.make_jcomm_reference(f, x, beta, EPS, precision="f32")
+    g = O.eval_joint_surrogate_cp(f, f, x, beta, slab=4)
+    d = O.D_beta(x, O.cp_reconstruct(f), beta)
+    assert abs(g - d) <= 1e-9 * (1.0 + d)
+    cur = [a.copy() for a in f]
+    for _ in range(2):
+        for n in range(3):
+            cur = ntf.jcomm_inner_update(cur, ctx, n, beta, EPS, precision="f32")
+            nxt = O.eval_joint_surrogate_cp(cur, f, x, beta, slab=4)
+            assert nxt <= g + 1e-6 * (1.0 + abs(g)), (n, g, nxt)
+            g = nxt
+    assert g >= O.D_beta(x, O.cp_reconstruct(cur), beta) - 1e-6 * (1.0 + abs(g))
