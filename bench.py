@@ -11,8 +11,9 @@ outer iteration: the J-CoMM reference pass (X -> P~, Q~, objective fused) and
 Q~ (51 GB) exceed the 126 MB L2 by 400x, so no flush is needed.
 
 The other BASELINE configs are measured as side keys of the same JSON line:
-C2 (512^3, R=32, all four betas), C1 (100^3 fp64 B-CoMM), C3 (Tucker 256^3,
-core 16^3) and C4 (sparse COO).
+C2 (512^3, R=32, all four betas, K3 roofline), C1 (100^3 fp64 B-CoMM), C3
+(Tucker 256^3, core 16^3, byte roofline) and C4 (sparse COO: byte model, e2e
+from host COO, densified-proxy CPU baseline).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -301,7 +302,7 @@ def run_c2(args, d: Dist):
             "per_beta": per_beta,
             "roofline_k3": {"bound": "hbm", "kernel": "tc_contract_kernel<32>", "achieved": ach, "peak": peak,
                             "unit": "GB/s", "frac": ach / peak, "peak_source": src, "avg_launch_ms": k3_ms,
-                            "algorithmic_bytes_per_launch": 8.0 * E},
+                            "algorithmic_bytes_per_launch": 8.0 * E, "traffic": ncu_traffic("c2_k3")[0]},
             "kernel_ms_per_outer": {"recon": pst["recon_ms"] / 2, "contract": pst["contract_ms"] / 2}}
 
 
@@ -357,9 +358,21 @@ def run_c3(args, d: Dist):
     ctx.set_profiling(False)
     del x
     torch.cuda.empty_cache()
+    E = float(np.prod(dims))
+    peak, src = peaks()
+    jm = out["jcomm_beta0.5"]["ms_per_iter"]
+    bm = out["bcomm_beta0.5"]["ms_per_iter"]
     return {"workload": "C3: Tucker 256^3 fp32, core 16^3, L=3 (BASELINE configs[2])", "fits": out,
             "jcomm_kernel_ms_one_outer": {"recon": pst["recon_ms"], "contract": pst["contract_ms"],
-                                          "other": pst["other_ms"]}}
+                                          "other": pst["other_ms"]},
+            "roofline": {"bound": "hbm", "peak": peak, "peak_source": src, "unit": "GB/s",
+                         "algorithmic_bytes_per_iter": {"bcomm": 4 * E * (1 + 3) * 3 + 4 * E * 4,
+                                                        "jcomm": 4 * E * (1 + 2 + 2 * 3 * 4)},
+                         "achieved": {"bcomm": (4 * E * (1 + 3) * 3 + 4 * E * 4) / (bm * 1e-3) / 1e9,
+                                      "jcomm": 4 * E * (1 + 2 + 2 * 3 * 4) / (jm * 1e-3) / 1e9},
+                         "note": "B-CoMM: per block (core + 3 factors) one reconstruction (X read, P and Q written) "
+                                 "and two E-sized rowgemm/contract passes; J-CoMM: SURVEY 8(d) s*E*(1+2+2L(1+N)). "
+                                 "Per-kernel times: profiles/r02_c3_launches.txt"}}
 
 
 C4_DIMS = (183, 24, 1140, 1717)
@@ -400,10 +413,67 @@ def run_c4(args, d: Dist):
     res = ntf.jcomm_fit_coo(di, dv, C4_DIMS, init, cfg(args.steps), ctx=ctx)
     st = ctx.stats()
     ms = st["device_ms"]
+    # e2e: host COO (numpy) through the public API, ingestion (merge + per-mode sort on the device),
+    # K outer iterations and the factor download inside the timed call
+    ntf.jcomm_fit_coo(idx, vals, C4_DIMS, init, cfg(1), ctx=ctx)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ntf.jcomm_fit_coo(idx, vals, C4_DIMS, init, cfg(args.steps), ctx=ctx)
+    e2e_s = time.perf_counter() - t0
+    fbytes = sum(a.size * 8 for a in init)
+    # byte model of one outer iteration (N1: each mode's numerator once per outer): every mode pass
+    # streams its sorted copy (4 int32 indices + fp64 value = 24 B per nonzero) and gathers N factor
+    # rows of R doubles per nonzero from L2
+    n, r, nnz = len(C4_DIMS), C4_RANK, C4_NNZ
+    stream_b = n * nnz * (4 * n + 8)
+    gather_b = n * nnz * n * r * 8
+    peak, src = peaks()
     return {"workload": "C4: sparse COO CP 183x24x1140x1717, 3.3M nnz (Zipf modes 2,3), R=20, beta=1, "
                         "J-CoMM L=3, fp64", "outer_it_per_s": args.steps / (ms * 1e-3),
             "ms_per_step": ms / args.steps, "final_loss": res.trace[-1].loss,
-            "gpu_launches": st["kernel_launches"]}
+            "gpu_launches": st["kernel_launches"],
+            "roofline": {"bound": "l2 gathers (working set 79 MB per sorted copy, factors 0.5 MB)",
+                         "streamed_bytes_per_outer": stream_b, "gathered_l2_bytes_per_outer": gather_b,
+                         "hbm_floor_ms": stream_b / (peak * 1e9) * 1e3, "hbm_peak_GBps": peak, "peak_source": src,
+                         "achieved_stream_GBps": stream_b / (ms / args.steps * 1e-3) / 1e9,
+                         "achieved_gather_GBps": gather_b / (ms / args.steps * 1e-3) / 1e9,
+                         "note": "SURVEY 8(d): L2/latency-bound, HBM is not binding; ncu L2 bytes of "
+                                 "coo_piece_kernel in profiles/r02_ncu_c4_coo_summary.txt"},
+            "e2e": {"value": args.steps / e2e_s, "unit": "outer_it/s",
+                    "h2d_bytes_per_step": int((idx.nbytes + vals.nbytes + fbytes) / args.steps),
+                    "d2h_bytes_per_step": int((fbytes + (args.steps + 1) * 24) / args.steps),
+                    "note": "host COO -> device ingestion (duplicate merge, per-mode sort) + K outer iterations + "
+                            "factor download in one public-API call"}}
+
+
+C4_PROXY_DIMS = (183, 24, 114, 172)  # modes 2,3 scaled by 1/10 -> 8.6e7 dense entries (<= 2^27)
+
+
+def c4_cpu_proxy():
+    """The reference cannot run C4 (dense 8.6e9 entries exceed read_coo's budget, io.cpp:109-110):
+    time ONE J-CoMM outer iteration of the compiled reference on a densified, down-scaled stand-in
+    with the same generator; reported as a proxy, per dense entry."""
+    from oracle import ref as R
+    if not R.available():
+        return None
+    rng = np.random.default_rng(0)
+    nnz = C4_NNZ // 10  # 10x C4's density: the dense reference's cost does not depend on it
+    x = np.zeros(C4_PROXY_DIMS)
+    cols = []
+    for m, dd in enumerate(C4_PROXY_DIMS):
+        if m >= 2:
+            w = 1.0 / np.arange(1, dd + 1) ** 1.1
+            cols.append(rng.choice(dd, size=nnz, p=w / w.sum()))
+        else:
+            cols.append(rng.integers(0, dd, size=nnz))
+    np.add.at(x, tuple(cols), 1.0 + (rng.geometric(0.5, size=nnz) - 1))
+    init = [0.1 + rng.random((dd, C4_RANK)) for dd in C4_PROXY_DIMS]
+    sec, _ = R.cp_time_outer("jcomm", x, init, 1.0, 1, inner_steps=C4_INNER)
+    return {"value": 1.0 / sec, "unit": "outer_it/s (proxy problem)", "cores": 1, "kind": "reference",
+            "sample": f"one J-CoMM outer iteration (beta=1, R=20, L=3) of the compiled reference on a densified "
+                      f"{'x'.join(map(str, C4_PROXY_DIMS))} stand-in ({int(np.prod(C4_PROXY_DIMS)):,} dense entries, "
+                      f"{nnz:,} draws, same generator); {sec:.2f} s. The reference has no sparse path and cannot "
+                      f"hold C4 densified (8.6e9 entries)"}
 
 
 def side(fn, *a):
@@ -537,6 +607,8 @@ def main():
             sides["c1"] = side(run_c1, args, d)
             sides["c3"] = side(run_c3, args, d)
             sides["c4_sparse"] = side(run_c4, args, d)
+            if not args.no_cpu_baseline and isinstance(sides["c4_sparse"], dict) and "error" not in sides["c4_sparse"]:
+                sides["c4_sparse"]["cpu_baseline_proxy"] = side(c4_cpu_proxy)
 
     if d.rank == 0:
         E = float(np.prod(C5_DIMS))
