@@ -189,3 +189,43 @@ def test_other_orders_vs_oracle(dims, ranks):
         res = fit(x, init, ntf.FitConfig(beta=1.5, ranks=ranks, max_iters=10, inner_steps=2))
         om, otr = ofit(x, init, O.FitConfig(beta=1.5, ranks=ranks, max_iters=10, inner_steps=2))
         assert rel_model(res.model, om) < 1e-10
+
+
+# Mid-size shapes that take the tiled kernels (tucker_kernels.cuh: cp.async rowgemm with
+# K % 32 == 0, split-b TTM with I_m >= 64 and J_m in {8, 16}, table-driven core pairing) and
+# the tcgen05 reconstruction with fp32 outputs and a row table (rows % 128 == 0, K % 128 == 0).
+def _tucker_problem(dims, ranks, seed):
+    rng = np.random.default_rng(seed)
+    core = rng.random(ranks)
+    fs = [rng.random((d, j)) for d, j in zip(dims, ranks)]
+    x = O.tucker_reconstruct(core, fs) * rng.gamma(10.0, 0.1, size=dims)
+    init = (0.1 + rng.random(ranks), [0.1 + rng.random((d, j)) for d, j in zip(dims, ranks)])
+    return x, init
+
+
+@pytest.mark.parametrize("algo", ["bcomm", "jcomm"])
+@pytest.mark.parametrize("beta", [0.5, 1.0, 1.5])
+@pytest.mark.parametrize("dims,ranks", [((64, 72, 128), (8, 16, 16)), ((16, 64, 256), (5, 8, 12))])
+def test_tucker_tiled_paths_match_oracle(algo, beta, dims, ranks):
+    x, init = _tucker_problem(dims, ranks, 3)
+    fit32 = ntf.tucker_bcomm_fit if algo == "bcomm" else ntf.tucker_jcomm_fit
+    ofit = O.tucker_bcomm_fit if algo == "bcomm" else O.tucker_jcomm_fit
+    om, otr = ofit(x, init, O.FitConfig(beta=beta, ranks=list(ranks), max_iters=4, inner_steps=2))
+    olosses = [t[2] for t in otr]
+    for prec, tf, tt in (("f64", 1e-10, 1e-10), ("f32", 1e-4, 1e-5)):
+        res = fit32(x, init, ntf.FitConfig(beta=beta, ranks=list(ranks), max_iters=4, inner_steps=2, precision=prec))
+        assert rel_model(res.model, om) < tf, prec
+        assert O.rel_err([t.loss for t in res.trace], olosses) < tt, prec
+
+
+def test_tucker_contractions_mid_size_vs_oracle():
+    # the split-b TTM and the offset-table core pairing against the oracle's einsum chains
+    rng = np.random.default_rng(9)
+    dims, ranks = (64, 80, 96), (8, 16, 8)
+    t = rng.random(dims)
+    fs = [rng.random((d, j)) + 0.05 for d, j in zip(dims, ranks)]
+    core = rng.random(ranks) + 0.05
+    assert O.rel_err(ntf.tucker_multimode_contract(t, fs), O.tucker_multimode_contract(t, fs)) < 1e-12
+    for mode in range(3):
+        assert O.rel_err(ntf.tucker_factor_contract(t, core, fs, mode),
+                         O.tucker_factor_contract(t, core, fs, mode)) < 1e-12
