@@ -102,10 +102,21 @@ static __global__ void coo_gather_kernel(const CooGatherParams p) {
   }
 }
 
-// nonzeros per key (integer atomics: deterministic counts)
+// nonzeros per key of a SORTED key array: the last element of each run finds
+// the run's first element by binary search (one atomicAdd per nonzero on a few
+// hundred hot addresses took 1.25 ms per mode at C4; this is a few microseconds)
 static __global__ void coo_count_kernel(const int32_t* keys, int64_t n, int32_t* cnt) {
-  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x)
-    atomicAdd(&cnt[keys[j]], 1);
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t k = keys[j];
+    if (j + 1 < n && keys[j + 1] == k) continue;
+    int64_t lo = 0, hi = j;  // first index with keys[idx] == k
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < k) lo = mid + 1;
+      else hi = mid;
+    }
+    cnt[k] = int32_t(j + 1 - lo);
+  }
 }
 
 static __global__ void coo_npieces_kernel(const int32_t* cnt, int64_t In, int64_t* np) {

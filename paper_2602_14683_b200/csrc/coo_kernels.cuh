@@ -109,6 +109,113 @@ static __global__ void __launch_bounds__(256) coo_piece_kernel(const CooPiecePar
   if (bad && p.flags) atomicOr(p.flags, bad);
 }
 
+// Lane-per-nonzero version (round 2).  ncu of the kernel above at C4: 73% issue
+// utilisation, 235 warp instructions per nonzero -- every nonzero costs the
+// whole warp two index shuffles per mode, a 10-shuffle fp64 warp sum and a
+// 20-of-32-lane gather.  Here a warp takes 32 nonzeros of its piece at once:
+//   phase 1 (lane = nonzero): Xhat = sum_r prod_m A_m(i_m, r) sequentially in r
+//           (each lane streams its own N factor rows: 16-byte loads, the
+//           second visit hits L1), p = x / max(Xhat, eps), and the off-mode
+//           products prod_{m != n} A_m(i_m, r) go to shared memory [32][R|1];
+//   phase 2 (lane = rank): acc(r) = fma(p_j, off_j(r), acc(r)) over the batch in
+//           nonzero order -- the same fma chain per rank as before.
+// No shuffles, no atomics; the summation order per (piece, rank) is unchanged,
+// Xhat is now a sequential sum over r (was a butterfly over lanes).
+constexpr int kCooWarps = 4;  // warps per CTA (shared memory: 32 x (R|1) doubles each)
+inline size_t coo_piece2_smem(int R) { return size_t(kCooWarps) * (size_t(32) * (R | 1) + 64) * sizeof(double); }
+
+static __global__ void __launch_bounds__(kCooWarps * 32) coo_piece2_kernel(const CooPieceParams p) {
+  extern __shared__ __align__(16) double coo_sm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int R = p.R, RS = R | 1;
+  double* off = coo_sm + size_t(w) * (size_t(32) * RS + 64);
+  double* pj = off + size_t(32) * RS;
+  double* tj = pj + 32;
+  const int64_t warp0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const bool vec = (R & 1) == 0;  // rows of R doubles start 16-byte aligned
+  unsigned bad = 0;
+  for (int64_t pc = warp0; pc < p.npieces; pc += nwarps) {
+    const int64_t j0 = p.piece_start[pc], j1 = p.piece_start[pc + 1];
+    double acc0 = 0.0, acc1 = 0.0, obj = 0.0;
+    for (int64_t jb = j0; jb < j1; jb += 32) {
+      const int cnt = int(j1 - jb < 32 ? j1 - jb : 32);
+      if (lane < cnt) {
+        const double* row[kMaxOrder];
+#pragma unroll
+        for (int m = 0; m < kMaxOrder; ++m)
+          row[m] = m < p.order ? p.fac[m] + int64_t(p.idx[m][jb + lane]) * R : nullptr;
+        const double x = p.val[jb + lane];
+        double y = 0.0;
+        if (vec) {
+#pragma unroll 2
+          for (int r = 0; r < R; r += 2) {
+            double2 a = __ldg(reinterpret_cast<const double2*>(row[0] + r));
+#pragma unroll
+            for (int m = 1; m < kMaxOrder; ++m) {
+              if (m >= p.order) break;
+              const double2 b = __ldg(reinterpret_cast<const double2*>(row[m] + r));
+              a.x *= b.x;
+              a.y *= b.y;
+            }
+            y += a.x;
+            y += a.y;
+          }
+        } else {
+          for (int r = 0; r < R; ++r) {
+            double a = __ldg(row[0] + r);
+#pragma unroll
+            for (int m = 1; m < kMaxOrder; ++m) {
+              if (m >= p.order) break;
+              a *= __ldg(row[m] + r);
+            }
+            y += a;
+          }
+        }
+        const double c = y < p.eps ? p.eps : y;  // std::max(xhat, eps)
+        pj[lane] = x / c;                        // weight_entries beta = 1 (kernels.hpp)
+        if (p.partial) {
+          double* orow = off + size_t(lane) * RS;
+          for (int r = 0; r < R; ++r) {
+            double o = 1.0;
+#pragma unroll
+            for (int m = 0; m < kMaxOrder; ++m) {
+              if (m >= p.order) break;
+              if (m != p.n) o *= __ldg(row[m] + r);
+            }
+            orow[r] = o;
+          }
+        }
+        if (p.obj) {
+          if (!(y > 0.0)) bad |= 1u;
+          if (x < 0.0) bad |= 2u;
+          tj[lane] = (x > 0.0 && y > 0.0) ? x * log(x / y) - x : 0.0;  // + y: closed form
+        }
+      }
+      __syncwarp();
+      if (p.partial) {
+        if (lane < R) {
+#pragma unroll 4
+          for (int t = 0; t < cnt; ++t) acc0 = fma(pj[t], off[size_t(t) * RS + lane], acc0);
+        }
+        if (lane + 32 < R) {
+#pragma unroll 4
+          for (int t = 0; t < cnt; ++t) acc1 = fma(pj[t], off[size_t(t) * RS + lane + 32], acc1);
+        }
+      }
+      if (p.obj && lane == 0)
+        for (int t = 0; t < cnt; ++t) obj += tj[t];
+      __syncwarp();
+    }
+    if (p.partial) {
+      if (lane < R) p.partial[pc * R + lane] = acc0;
+      if (lane + 32 < R) p.partial[pc * R + lane + 32] = acc1;
+    }
+    if (p.obj && lane == 0) p.obj[pc] = obj;
+  }
+  if (bad && p.flags) atomicOr(p.flags, bad);
+}
+
 // Num(k, r) = sum of the pieces of key k: 8 warps take pieces k0 + w, k0 + w + 8,
 // ... in order, then warps combine in order (fixed shape => deterministic).
 static __global__ void __launch_bounds__(256) coo_key_reduce_kernel(const double* partial, const int64_t* key_piece,

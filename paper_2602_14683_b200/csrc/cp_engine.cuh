@@ -1107,10 +1107,24 @@ class CpEngine {
     pp.partial = partials ? coo_partial_ : nullptr;
     pp.obj = objective ? coo_obj_ : nullptr;
     pp.flags = flags_;
-    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(cm.npieces, 8), int64_t(c_.sm_count) * 16)));
     const int ph = c_.prof_begin(1);
-    if (R_ <= 32) coo_piece_kernel<1><<<grid, 256, 0, c_.stream>>>(pp);
-    else coo_piece_kernel<2><<<grid, 256, 0, c_.stream>>>(pp);
+    static const bool old_kernel = [] { const char* e = std::getenv("NTFG_COO_WARP_PER_NNZ"); return e && e[0] == '1'; }();
+    if (old_kernel) {  // round-1 kernel (one warp per nonzero), kept for A/B timing
+      const int grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(cm.npieces, 8), int64_t(c_.sm_count) * 16)));
+      if (R_ <= 32) coo_piece_kernel<1><<<grid, 256, 0, c_.stream>>>(pp);
+      else coo_piece_kernel<2><<<grid, 256, 0, c_.stream>>>(pp);
+    } else {
+      const size_t sm = coo_piece2_smem(int(R_));
+      static size_t attr = 48 * 1024;
+      if (sm > attr) {
+        cuda_check(cudaFuncSetAttribute(coo_piece2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),
+                   "cudaFuncSetAttribute");
+        attr = sm;
+      }
+      const int grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(cm.npieces, kCooWarps),
+                                                                 int64_t(c_.sm_count) * 16)));
+      coo_piece2_kernel<<<grid, kCooWarps * 32, sm, c_.stream>>>(pp);
+    }
     NTFG_LAUNCHED(c_);
     c_.prof_end(ph);
   }
