@@ -82,6 +82,7 @@ class CpEngine {
     // objective partials: one per recon CTA (grid depends on the kernel variant)
     objpart_ = c_.buf<double>("cp.objpart", size_t(std::max({recon_grid(false), recon_grid(true), c_.sm_count * 8})));
     tc_ = decide_tc();
+    if (sizeof(T) == 4 && N_ >= 2) hstage_ = c_.buf<float>("cp.hstage", size_t(g_.dims[N_ - 2]) * size_t(R_));
   }
 
   int order() const { return N_; }
@@ -261,6 +262,17 @@ class CpEngine {
       const int64_t ntiles = g_.rows / kRcRows;
       const int64_t per = std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(c_.sm_count) / p.ktiles));
       recon_grid_ = int(per * p.ktiles);
+      if constexpr (sizeof(T) == 4) {
+        // fp32 copy of the fastest row mode's factor for the H producers: pays at R = 64 (C5 K2 12.3 ->
+        // 11.8 ms, half the L2 bytes per tile), not at R = 32 (C2 0.327 -> 0.361 ms), measured
+        if (!htab && hstage_ && (R_ & 3) == 0 && R_ > 32) {
+          const int64_t n = g_.dims[N_ - 2] * R_;
+          stage_kernel<float><<<int(ceil_div(n, 256)), 256, 0, c_.stream>>>(fac[N_ - 2], g_.dims[N_ - 2], int(R_),
+                                                                            int(R_), hstage_);
+          NTFG_LAUNCHED(c_);
+          p.hfac32 = hstage_;
+        }
+      }
       const int ph = c_.prof_begin(0);
       if constexpr (sizeof(T) == 4) {
         recon_tc_launch(recon_grid_, c_.stream, p, RP_, bk_);
@@ -1426,6 +1438,7 @@ class CpEngine {
   bool planes_out_ = false;
   void* planes_[4] = {nullptr, nullptr, nullptr, nullptr};
   float* lastT_ = nullptr;
+  float* hstage_ = nullptr;   // fp32 copy of the fastest row mode's factor (recon_tc H producers)
   unsigned* flags_;
   int* counter_;
   int recon_grid_ = 0;

@@ -94,6 +94,7 @@ struct ReconParams {
   const double* fac[kMaxOrder];  // model factors (fp64) for the prefix product H
   const double* htab;            // nullable: H(row, r) = htab[row * R + r] (Tucker partial chain)
   const T* alast;                // staged last factor, [K][RP] (zero padded)
+  const float* hfac32;           // nullable: fp32 copy [I_f][R] of the fastest row mode's factor (recon_tc H producers)
   const T* x;
   T* pout;                       // nullable
   T* qout;                       // nullable

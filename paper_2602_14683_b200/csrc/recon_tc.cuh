@@ -191,7 +191,39 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
       // factor, or (Tucker partial chain) of the row table itself
       const double* hsrc = p.htab ? p.htab + row0 * R : p.fac[f] + p.g.coord(row0, f) * R;
       const uint32_t hhi = hbase + st * 2u * plane, hlo = hhi + plane;
-      if ((R & 3) == 0) {
+      if ((R & 3) == 0 && p.hfac32 && !p.htab) {
+        // fp32 staged factor: one 16-byte load per item, fp32 product with the
+        // (fp64-accumulated, then rounded) slower-mode product G
+        const int R4 = R >> 2;
+        const int kstep = PT % R4, rowstep4 = PT / R4, nchunk = kRcRows * R4;
+        const float4* fr = reinterpret_cast<const float4*>(p.hfac32 + p.g.coord(row0, f) * R);
+        int row = pt / R4, kc = pt - row * R4;
+#pragma unroll 4
+        for (int c = pt; c < nchunk; c += PT) {
+          const float4 v4 = __ldg(fr + c);
+          float v[4] = {v4.x, v4.y, v4.z, v4.w};
+          if (npre >= 2) {
+            const double2 g01 = *reinterpret_cast<const double2*>(&gs[st][4 * kc]);
+            const double2 g23 = *reinterpret_cast<const double2*>(&gs[st][4 * kc + 2]);
+            v[0] *= float(g01.x); v[1] *= float(g01.y); v[2] *= float(g23.x); v[3] *= float(g23.y);
+          }
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            hi[e] = tf32_rna(v[e]);
+            lo[e] = tf32_rna(v[e] - __uint_as_float(hi[e]));
+          }
+          const uint32_t off = uint32_t(row >> 3) * sbo + uint32_t(kc) * kRcLbo + uint32_t(row & 7) * 16u;
+          tc::sts_v4(hhi + off, make_uint4(hi[0], hi[1], hi[2], hi[3]));
+          tc::sts_v4(hlo + off, make_uint4(lo[0], lo[1], lo[2], lo[3]));
+          kc += kstep;
+          row += rowstep4;
+          if (kc >= R4) {
+            kc -= R4;
+            ++row;
+          }
+        }
+      } else if ((R & 3) == 0) {
         // four consecutive ranks of one row per item: 32-byte loads (a warp
         // reads 1 KB contiguous), one 16-byte store per plane (conflict-free
         // with the 144-byte core-matrix stride), one address per four values
