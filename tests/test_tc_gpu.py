@@ -174,3 +174,17 @@ def test_tc_inner_updates_descend_the_joint_surrogate(beta):
             assert nxt <= g + 1e-6 * (1.0 + abs(g)), (n, g, nxt)
             g = nxt
     assert g >= O.D_beta(x, O.cp_reconstruct(cur), beta) - 1e-6 * (1.0 + abs(g))
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5, 1.0, 1.5])
+def test_recon_tc_fp32_outputs_with_cuda_core_contraction(beta, monkeypatch):
+    # NTFG_DISABLE_TC=1 keeps the CUDA-core contraction (fp32 P~/Q~ arrays); the reconstruction still
+    # runs on tcgen05 and writes those arrays directly
+    x, init = problem((4, 128, 128), 12, 31)
+    monkeypatch.setenv("NTFG_DISABLE_TC", "1")
+    cfg = ntf.FitConfig(beta=beta, rank=12, max_iters=6, inner_steps=2, precision="f32")
+    for fit, ofit in ((ntf.jcomm_fit, O.jcomm_fit), (ntf.bcomm_fit, O.bcomm_fit)):
+        res = fit(x, init, cfg)
+        om, otr = ofit(x, init, O.FitConfig(beta=beta, rank=12, max_iters=6, inner_steps=2))
+        assert relm(res.model, om) < 1e-4
+        assert O.rel_err([t.loss for t in res.trace], [t[2] for t in otr]) < 1e-5

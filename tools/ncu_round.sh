@@ -30,6 +30,7 @@ full() {  # name regex skip cmd...
   ncu -i $out/$name.ncu-rep --page raw --csv > $out/$name.raw.csv 2>/dev/null
   rm -f $out/$name.sass.csv $out/$name.ncu-rep
 }
+list bench python bench.py --steps 2 --warmup 3 --no-side --no-e2e --no-cpu-baseline
 list c5 python tools/prof_c5.py 1
 list c2_b05 python tools/prof_c2.py 0.5 1
 list c2_b1 python tools/prof_c2.py 1.0 1
@@ -63,5 +64,6 @@ for f in sorted(glob.glob(out+"/*.raw.csv")):
 json.dump(res, open(out+"/ncu_traffic.json","w"), indent=1)
 print(json.dumps(res, indent=1))
 PY
+[ -x tools/mma_probe ] || nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_probe tools/mma_probe.cu -lcuda
 ./tools/mma_probe > $out/mma_probe.txt 2>&1
 for f in $out/*.summary.txt $out/*.launches.txt; do echo "=== $f"; head -30 $f; done
