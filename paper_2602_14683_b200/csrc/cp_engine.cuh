@@ -527,6 +527,8 @@ class CpEngine {
       p.gfast = (f >= 0 && g_.dims[f] % kTcRows == 0) ? 1 : 0;
       const char* slow = std::getenv("NTFG_TC_SLOW_GATHER");  // tests: force the per-row gather path
       if (slow && slow[0] == '1') p.gfast = 0;
+      p.fmode = f;
+      p.btiles = btiles_;  // scratch for the static B tiles (decided by the launcher)
     }
     p.lay = tc_layout(ns, p.N, nmm, p.gfast != 0);
     p.partA = reinterpret_cast<float*>(partA_);
@@ -636,6 +638,11 @@ class CpEngine {
       size_t fl = 0;
       for (int m = 0; m < N_; ++m) fl += size_t(g_.dims[m]) * 64;
       lastT_ = c_.buf<float>("cp.lastT", 2 * fl);
+      // static B tiles: [2 streams][I_f / 16 blocks][hi, lo][(N / 8) * 272 B] for the largest row mode
+      int64_t imax = 16;
+      for (int m = 0; m < N_ - 1; ++m) imax = std::max<int64_t>(imax, g_.dims[m]);
+      btiles_ = static_cast<unsigned char*>(c_.bufs.get("cp.btiles", size_t(2) * size_t(ceil_div(imax, 16)) * 2 *
+                                                                       size_t(tc_n() / 8 * kTcBSbo)));
     }
     ensure_pq();
   }
@@ -1438,6 +1445,7 @@ class CpEngine {
   bool planes_out_ = false;
   void* planes_[4] = {nullptr, nullptr, nullptr, nullptr};
   float* lastT_ = nullptr;
+  unsigned char* btiles_ = nullptr;  // static B tiles of the tensor-core contraction (tc_contract.cuh)
   float* hstage_ = nullptr;   // fp32 copy of the fastest row mode's factor (recon_tc H producers)
   unsigned* flags_;
   int* counter_;

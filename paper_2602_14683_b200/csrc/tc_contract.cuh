@@ -55,7 +55,7 @@ template <int N> __host__ __device__ constexpr int tc_bwarps() { return N > 32 ?
 template <int N> __host__ __device__ constexpr int tc_threads() { return 32 * (tc_bwarps<N>() + 7 + (tc_issuers<N>() - 1)); }
 constexpr int kTcBSbo = 272;    // bytes between 8-column groups of a B tile (256 + 16: bank spread)
 constexpr int kTcGModes = 3;    // factor modes gathered through the cp.async ring (more: direct fp64)
-constexpr size_t kTcSmemMax = 227 * 1024 - 5120;  // dynamic budget (static smem 4.3 KB + 1 KB alignment slack)
+constexpr size_t kTcSmemMax = 227 * 1024 - 6144;  // dynamic budget (static smem 5.4 KB + alignment slack)
 
 // runtime shared-memory layout (host-computed, tc_layout)
 struct TcLayout {
@@ -85,6 +85,13 @@ struct TcParams {
                              // is an fp32 MMA result, so fp32 F adds ~6e-8 per term)
   const float* fac32[2][kMaxOrder];  // every factor as [I_m][N] fp32, zero padded (B operand gathers)
   int gfast;                          // stage rows = 16 consecutive rows of the fastest off-mode
+  // static B tiles (sb): the B operand of a stage is the bf16 hi/lo split of 16 rows of the
+  // fastest off-mode's factor alone -- built ONCE per launch in global memory in the tile
+  // layout and bulk-copied per stage -- and the product g(r) of the other off-modes' rows,
+  // constant over a run of I_f rows, scales the finished segment in the epilogue
+  // (segments end at run boundaries).  No B-producer or gather work per stage.
+  int sb, sb_runst, fmode;            // enabled, stages per run (I_f / 16), fastest off-mode
+  unsigned char* btiles;              // [ns][I_f / 16][hi, lo][b_tile] (engine scratch)
   TcLayout lay;
   float* partA;          // [ns][units][K][RP]
   double* partB;         // [ns][In][S][RP]
@@ -126,6 +133,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   __shared__ uint64_t g_full[kTcMaxGather], g_empty[kTcMaxGather];
   __shared__ uint32_t tmem_base;
   __shared__ double red[4][128];
+  __shared__ float gsm[2][128];  // static-B mode: run scale g per (stream, rank), double-buffered by segment
 
   // warp index through a shuffle: the compiler then treats the role branches
   // (and everything computed inside them from uniform inputs) as warp-uniform
@@ -207,6 +215,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         const int blk0 = int(w % p.G) * 2 * p.mtw;  // first 64-column block of this item's m-tiles
         int64_t j0, j1, itgt, split;
         unit_range(u, j0, j1, itgt, split);
+        int rblk = p.sb ? int((j0 / kTcRows) % p.sb_runst) : 0;  // 16-row block of the fastest off-mode
         for (int64_t j = j0; j < j1; j += kTcRows) {
           const unsigned long long tq = p.trace ? clock64() : 0;
           tc::wait(&empty[slot], sph);
@@ -219,12 +228,17 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
             c2 = int(j - aa * p.Bn); c3 = int(itgt); c4 = int(aa);
           }
           if (tc::elect_one()) {
-            tc::expect_tx(&a_full[slot], bytes);
+            tc::expect_tx(&a_full[slot], bytes + (p.sb ? unsigned(p.ns) * 2u * L.b_tile : 0u));
             for (int s = 0; s < p.ns; ++s)
               for (int plane = 0; plane < 2; ++plane)
                 tc::tma_load_5d(stage_a(slot, s, plane), &maps.m[s][plane], 0, c2, c3, c4, blk0, &a_full[slot]);
+            if (p.sb)  // this stage's 16 factor rows as ready-made hi/lo B tiles (adjacent in smem)
+              for (int s = 0; s < p.ns; ++s)
+                tma::bulk_g2s(stage_b(slot, s, 0), p.btiles + size_t((s * p.sb_runst + rblk) * 2) * L.b_tile,
+                              2u * L.b_tile, &a_full[slot]);
           }
           __syncwarp();
+          if (++rblk == p.sb_runst) rblk = 0;
           if (++slot == L.nst) {
             slot = 0;
             sph ^= 1u;
@@ -267,11 +281,13 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
       unit_range(w / p.G, j0, j1, itgt, split);
       const int nstage = int((j1 - j0 + kTcRows - 1) / kTcRows);
       int qi = 0;
+      int rblk = p.sb ? int((j0 / kTcRows) % p.sb_runst) : 0;
       for (int stg = 0; stg < nstage; ++stg) {
         const bool seg_first = qi == 0;
-        const bool seg_last = qi == p.seg - 1 || stg == nstage - 1;
+        const bool seg_last = qi == p.seg - 1 || stg == nstage - 1 || (p.sb && rblk == p.sb_runst - 1);
+        if (++rblk == p.sb_runst) rblk = 0;
         tc::wait(&a_full[slot], sph);
-        tc::wait(&b_full[slot], sph);
+        if (!p.sb) tc::wait(&b_full[slot], sph);
         tc::fence_after_sync();
         for (int t = issuer; t < ntile; t += tc_issuers<NMAX>()) {
           const int s = t >= p.mtw ? 1 : 0, m = t - s * p.mtw;
@@ -332,7 +348,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     int gs = 0;
     uint32_t gph = 1;  // producer parity: the first pass finds every gather slot free
     unsigned long long gw = 0, g00 = p.trace ? clock64() : 0;
-    if (gm > 0 && !(p.ablate & 1)) {
+    if (gm > 0 && !(p.ablate & 1) && !p.sb) {
       for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
         int64_t j0, j1, itgt, split;
         unit_range(w / p.G, j0, j1, itgt, split);
@@ -395,7 +411,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     int slot = -1, gs = -1;           // ring positions (advanced at the top of every stage)
     uint32_t sph = 0, gph = 1;        // sph: parity the slot's "empty" wait uses (ph ^ 1 trick); gph: gather "full" parity
     unsigned long long bw0 = 0, bw1 = 0, b00 = p.trace ? clock64() : 0;
-    for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
+    for (int64_t w = blockIdx.x; w < p.items && !p.sb; w += gridDim.x) {
       int64_t j0, j1, itgt, split;
       unit_range(w / p.G, j0, j1, itgt, split);
       for (int64_t jb = j0; jb < j1; jb += kTcRows) {
@@ -498,25 +514,64 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     const uint32_t lanes = uint32_t(quarter * 32) << 16;
     const uint32_t run = tmem + lanes + uint32_t(cols_per_buf);
     const uint32_t sbuf = tmem + lanes;
+    // static-B mode: g(r) = product of the other off-modes' rows (ascending,
+    // fp32) for the run a segment belongs to; thread et owns entry
+    // (stream et / N, rank et % N), prefetched one segment ahead
+    const int nrm = p.g.order - 1;
+    int om[kMaxOrder];
+    int nom = 0;  // off-modes other than the fastest one
+    for (int m = 0; m < nrm; ++m)
+      if (m != p.n && m != p.fmode) om[nom++] = m;
+    const bool has_g = p.sb && nom > 0;
+    auto g_of = [&](int64_t j, int64_t itgt) -> float {
+      if (!has_g || et >= p.ns * N) return 1.f;
+      const int s = et / N, r = et - s * N;
+      const int64_t row = row_of(j, itgt);
+      float gv = __ldg(p.fac32[s][om[0]] + p.g.coord(row, om[0]) * N + r);
+      for (int q = 1; q < nom; ++q) gv *= __ldg(p.fac32[s][om[q]] + p.g.coord(row, om[q]) * N + r);
+      return gv;
+    };
     uint32_t sc = 0;
     for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
       const int64_t u = w / p.G;
       const int g = int(w % p.G);
       int64_t j0, j1, itgt, split;
       unit_range(u, j0, j1, itgt, split);
-      const int64_t nstage = (j1 - j0 + kTcRows - 1) / kTcRows;
-      const int64_t nseg = (nstage + p.seg - 1) / p.seg;
-      for (int64_t sg = 0; sg < nseg; ++sg, ++sc) {
+      const int nstage = int((j1 - j0 + kTcRows - 1) / kTcRows);
+      int qi = 0, sg = 0;
+      int rblk = p.sb ? int((j0 / kTcRows) % p.sb_runst) : 0;
+      float gnext = g_of(j0, itgt);
+      for (int stg = 0; stg < nstage; ++stg) {
+        const bool seg_last = qi == p.seg - 1 || stg == nstage - 1 || (p.sb && rblk == p.sb_runst - 1);
+        if (++rblk == p.sb_runst) rblk = 0;
+        if (!seg_last) {
+          ++qi;
+          continue;
+        }
+        qi = 0;
+        const float* gcur = gsm[sc & 1u];
+        if (has_g) {
+          gsm[sc & 1u][et] = gnext;
+          if (stg + 1 < nstage) gnext = g_of(j0 + int64_t(stg + 1) * kTcRows, itgt);  // next segment's run
+          named_sync(1, 128);
+        }
         for (int t = 0; t < ntile; ++t) {
           tc::wait(&acc_full[t], sc & 1u);
           tc::fence_after_sync();
           if (!(p.ablate & 4)) {
+            const int gbase = (t / p.mtw) * N - t * N;  // column c * 16 + j of tile t -> entry (stream, rank)
             for (int c = t * (N / 16); c < (t + 1) * (N / 16); ++c) {
               uint32_t v[16], r[16];
               tc::tmem_ld16_nowait(sbuf + uint32_t(c * 16), v);
               if (sg > 0) tc::tmem_ld16_nowait(run + uint32_t(c * 16), r);
               tc::tmem_ld_wait();
-              if (sg > 0) {
+              if (has_g) {
+                const float* gp = gcur + gbase + c * 16;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  v[j] = __float_as_uint(sg > 0 ? fmaf(__uint_as_float(v[j]), gp[j], __uint_as_float(r[j]))
+                                                : __uint_as_float(v[j]) * gp[j]);
+              } else if (sg > 0) {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(v[j]));
               }
@@ -527,6 +582,8 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
           tc::warp_arrive(&acc_empty[t], lane);  // the segment tile is read: its next segment may start
         }
         tc::tmem_st_wait();
+        ++sc;
+        ++sg;
       }
       if (p.ablate & 4) continue;
       if (p.caseA) {
