@@ -201,6 +201,38 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     return smem + L.b_off + ((size_t(slot) * 2 + s) * 2 + plane) * L.b_tile;
   };
 
+  unsigned long long ew_out = 0, ed_out = 0;
+  // Drain groups (static-B mode): the idle B-producer warps form kB / 4 extra
+  // groups of four warps (one per TMEM lane quarter) next to the epilogue
+  // warps; group q drains the segment tiles t = q, q + ngroups, ...  A tile's
+  // drain is ~1200 cycles of TMEM round trips, and the issuer cannot start a
+  // tile's next segment before it is drained: draining the tiles in parallel
+  // cut the issuer's wait from 14% of the launch.
+  const int ngroups = p.sb ? 1 + kB / 4 : 1;
+  const int ntile_all = p.ns * p.mtw;
+  const uint32_t cols_run = uint32_t(cols_per_buf);
+  // one segment tile into the running sums: run = (sg ? run : 0) + seg * g
+  auto drain_tile = [&](int t, bool first, bool has_g, const float* gcur, uint32_t lanes_) {
+    const uint32_t sbuf_ = tmem + lanes_, run_ = tmem + lanes_ + cols_run;
+    const int gbase = (t / p.mtw) * N - t * N;  // column c * 16 + j of tile t -> entry (stream, rank)
+    for (int c = t * (N / 16); c < (t + 1) * (N / 16); ++c) {
+      uint32_t v[16], r[16];
+      tc::tmem_ld16_nowait(sbuf_ + uint32_t(c * 16), v);
+      if (!first) tc::tmem_ld16_nowait(run_ + uint32_t(c * 16), r);
+      tc::tmem_ld_wait();
+      if (has_g) {
+        const float* gp = gcur + gbase + c * 16;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          v[j] = __float_as_uint(!first ? fmaf(__uint_as_float(v[j]), gp[j], __uint_as_float(r[j]))
+                                        : __uint_as_float(v[j]) * gp[j]);
+      } else if (!first) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(v[j]));
+      }
+      tc::tmem_st16(run_ + uint32_t(c * 16), v);
+    }
+  };
   if (warp == kWTma) {
     // ================= TMA producer =================
     // converged warp, one elected lane issues (uniform operands: no per-lane
@@ -276,6 +308,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     const uint32_t a_plane16 = (L.a_stream / 2) >> 4, b_tile16 = L.b_tile >> 4;
     int slot = 0;
     uint32_t sph = 0, sc = 0;
+    unsigned long long iw = 0;  // trace: cycles this issuer waited for segment drains
     for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
       int64_t j0, j1, itgt, split;
       unit_range(w / p.G, j0, j1, itgt, split);
@@ -292,7 +325,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         for (int t = issuer; t < ntile; t += tc_issuers<NMAX>()) {
           const int s = t >= p.mtw ? 1 : 0, m = t - s * p.mtw;
           if (seg_first) {  // the epilogue drained this tile's previous segment
+            const unsigned long long tq = p.trace ? clock64() : 0;
             tc::wait(&acc_empty[t], (sc & 1u) ^ 1u);
+            if (p.trace) iw += clock64() - tq;
             tc::fence_after_sync();
           }
           const uint32_t aoff = uint32_t(slot) * L.a_stage + uint32_t(s) * L.a_stream + uint32_t(m) * 4096u;
@@ -324,6 +359,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         }
       }
     }
+    if (p.trace && p.sb && lane == 0 && issuer == 0) p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 2] = iw;
   } else if (warp == kWGather) {
     // ================= factor-row gathers (bulk async copies) =================
     // gather slot q % gdepth holds, per stream, gm regions of [16][N] floats.
@@ -495,7 +531,50 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         tc::warp_arrive(&b_full[slot], lane);
       }
     }
-    if (p.trace && tid == 0) {
+    if (p.sb) {
+      // ---- helper drain group (see drain_tile): warps 4q .. 4q+3 are group q + 1
+      const int grp = 1 + warp / 4;
+      const uint32_t lanes_ = uint32_t((warp & 3) * 32) << 16;
+      int om_n = 0;
+      for (int m = 0; m < nrm; ++m)
+        if (m != p.n && m != p.fmode) ++om_n;
+      const bool has_g = om_n > 0;
+      uint32_t sc = 0;
+      for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
+        int64_t j0, j1, itgt, split;
+        unit_range(w / p.G, j0, j1, itgt, split);
+        const int nstage = int((j1 - j0 + kTcRows - 1) / kTcRows);
+        int qi = 0, sg = 0;
+        int rblk = int((j0 / kTcRows) % p.sb_runst);
+        for (int stg = 0; stg < nstage; ++stg) {
+          const bool seg_last = qi == p.seg - 1 || stg == nstage - 1 || rblk == p.sb_runst - 1;
+          if (++rblk == p.sb_runst) rblk = 0;
+          if (!seg_last) {
+            ++qi;
+            continue;
+          }
+          qi = 0;
+          if (has_g) named_sync(3, 128 * ngroups);  // the epilogue group published this segment's g
+          for (int t = grp; t < ntile_all; t += ngroups) {
+            tc::wait(&acc_full[t], sc & 1u);
+            tc::fence_after_sync();
+            drain_tile(t, sg == 0, has_g, gsm[sc & 1u], lanes_);
+            tc::fence_before_sync();
+            tc::warp_arrive(&acc_empty[t], lane);
+          }
+          tc::tmem_st_wait();
+          ++sc;
+          ++sg;
+        }
+        // the epilogue group reads the running sums of every tile: after every group's
+        // last drain (first barrier), and before anyone overwrites them (second barrier)
+        tc::fence_before_sync();
+        named_sync(3, 128 * ngroups);
+        named_sync(3, 128 * ngroups);
+        tc::fence_after_sync();
+      }
+    }
+    if (p.trace && !p.sb && tid == 0) {
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 0] = bw0;
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 1] = bw1;
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 2] = clock64() - b00;
@@ -532,6 +611,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
       return gv;
     };
     uint32_t sc = 0;
+    unsigned long long ew = 0, ed = 0;  // trace: cycles waiting for a finished segment tile / draining it
     for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
       const int64_t u = w / p.G;
       const int g = int(w % p.G);
@@ -553,39 +633,37 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         if (has_g) {
           gsm[sc & 1u][et] = gnext;
           if (stg + 1 < nstage) gnext = g_of(j0 + int64_t(stg + 1) * kTcRows, itgt);  // next segment's run
-          named_sync(1, 128);
+          named_sync(ngroups > 1 ? 3 : 1, 128 * ngroups);
         }
-        for (int t = 0; t < ntile; ++t) {
+        for (int t = 0; t < ntile; t += ngroups) {
+          const unsigned long long tq0 = p.trace ? clock64() : 0;
           tc::wait(&acc_full[t], sc & 1u);
           tc::fence_after_sync();
-          if (!(p.ablate & 4)) {
-            const int gbase = (t / p.mtw) * N - t * N;  // column c * 16 + j of tile t -> entry (stream, rank)
-            for (int c = t * (N / 16); c < (t + 1) * (N / 16); ++c) {
-              uint32_t v[16], r[16];
-              tc::tmem_ld16_nowait(sbuf + uint32_t(c * 16), v);
-              if (sg > 0) tc::tmem_ld16_nowait(run + uint32_t(c * 16), r);
-              tc::tmem_ld_wait();
-              if (has_g) {
-                const float* gp = gcur + gbase + c * 16;
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                  v[j] = __float_as_uint(sg > 0 ? fmaf(__uint_as_float(v[j]), gp[j], __uint_as_float(r[j]))
-                                                : __uint_as_float(v[j]) * gp[j]);
-              } else if (sg > 0) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(v[j]));
-              }
-              tc::tmem_st16(run + uint32_t(c * 16), v);
-            }
+          if (p.trace) {
+            const unsigned long long tq1 = clock64();
+            ew += tq1 - tq0;
+            ed -= tq1;
           }
+          if (!(p.ablate & 4)) drain_tile(t, sg == 0, has_g, gcur, lanes);
           tc::fence_before_sync();
           tc::warp_arrive(&acc_empty[t], lane);  // the segment tile is read: its next segment may start
+          if (p.trace) ed += clock64();
         }
         tc::tmem_st_wait();
+        ew_out = ew;
+        ed_out = ed;
         ++sc;
         ++sg;
       }
-      if (p.ablate & 4) continue;
+      if (ngroups > 1) {  // every group's last drain of this item is in the running sums
+        tc::fence_before_sync();
+        named_sync(3, 128 * ngroups);
+        tc::fence_after_sync();
+      }
+      if (p.ablate & 4) {
+        if (ngroups > 1) named_sync(3, 128 * ngroups);
+        continue;
+      }
       if (p.caseA) {
         for (int t = 0; t < ntile; ++t) {
           const int s = t / p.mtw, m = t - s * p.mtw;
@@ -655,7 +733,15 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         }
         named_sync(1, 128);
       }
+      if (ngroups > 1) {  // running sums read: the groups may start the next item's first segment
+        tc::fence_before_sync();
+        named_sync(3, 128 * ngroups);
+      }
     }
+  }
+  if (p.trace && p.sb && tid == kB * 32) {  // static-B mode: the B counters' slots carry the epilogue's
+    p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 0] = ew_out;
+    p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 1] = ed_out;
   }
   tc::fence_before_sync();
   __syncthreads();

@@ -17,3 +17,4 @@ for hdr, ws in launches[: int(sys.argv[2]) if len(sys.argv) > 2 else 6]:
     m = [int(S.median([w[i] for w in ws])) for i in range(7)]
     print(hdr)
     print("  B: wait g_full %d  wait empty %d  total %d | gather: wait g_empty %d  total %d | TMA: wait empty %d  total %d" % tuple(m))
+    print("  (static-B launches: the three B slots are the epilogue's wait for finished tiles, its drain cycles, and the issuer's wait for drains)")
