@@ -215,22 +215,29 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   auto drain_tile = [&](int t, bool first, bool has_g, const float* gcur, uint32_t lanes_) {
     const uint32_t sbuf_ = tmem + lanes_, run_ = tmem + lanes_ + cols_run;
     const int gbase = (t / p.mtw) * N - t * N;  // column c * 16 + j of tile t -> entry (stream, rank)
-    for (int c = t * (N / 16); c < (t + 1) * (N / 16); ++c) {
-      uint32_t v[16], r[16];
-      tc::tmem_ld16_nowait(sbuf_ + uint32_t(c * 16), v);
-      if (!first) tc::tmem_ld16_nowait(run_ + uint32_t(c * 16), r);
+    constexpr int CW = (N == 64) ? 32 : 16;  // columns per TMEM round trip (x32 only paid at N = 64, measured)
+    for (int c = t * (N / CW); c < (t + 1) * (N / CW); ++c) {
+      uint32_t v[CW], r[CW];
+      if constexpr (CW == 32) {
+        tc::tmem_ld32_nowait(sbuf_ + uint32_t(c * CW), v);
+        if (!first) tc::tmem_ld32_nowait(run_ + uint32_t(c * CW), r);
+      } else {
+        tc::tmem_ld16_nowait(sbuf_ + uint32_t(c * CW), v);
+        if (!first) tc::tmem_ld16_nowait(run_ + uint32_t(c * CW), r);
+      }
       tc::tmem_ld_wait();
       if (has_g) {
-        const float* gp = gcur + gbase + c * 16;
+        const float* gp = gcur + gbase + c * CW;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < CW; ++j)
           v[j] = __float_as_uint(!first ? fmaf(__uint_as_float(v[j]), gp[j], __uint_as_float(r[j]))
                                         : __uint_as_float(v[j]) * gp[j]);
       } else if (!first) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(v[j]));
+        for (int j = 0; j < CW; ++j) v[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(v[j]));
       }
-      tc::tmem_st16(run_ + uint32_t(c * 16), v);
+      if constexpr (CW == 32) tc::tmem_st32(run_ + uint32_t(c * CW), v);
+      else tc::tmem_st16(run_ + uint32_t(c * CW), v);
     }
   };
   if (warp == kWTma) {
