@@ -43,7 +43,7 @@ full c2_k3 tc_contract_kernel 1 python tools/prof_c2.py 0.5 1
 full c2_k2 recon_tc_kernel 0 python tools/prof_c2.py 0.5 1
 full c3_rowgemm rowgemm_tiled_kernel 1 python tools/prof_c3.py jcomm 0.5 1
 full c3_recon recon_tc_kernel 0 python tools/prof_c3.py jcomm 0.5 1
-full c4_coo coo_piece_kernel 4 python tools/prof_c4.py 2
+full c4_coo coo_piece 4 python tools/prof_c4.py 2
 python - $out <<'PY'
 import csv, json, sys, os, glob
 out=sys.argv[1]; res={}
