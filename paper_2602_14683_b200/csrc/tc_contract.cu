@@ -46,6 +46,8 @@ void tc_contract_launch(int grid, cudaStream_t stream, const TcMaps& maps, const
   static const bool sb_off = [] { const char* e = std::getenv("NTFG_TC_STATIC_B"); return e && e[0] == '0'; }();
   p.sb = 0;
   p.sb_runst = 0;
+  // (at N <= 32 the producer warps kept up, so the gain there is only the saved SM work: C2 step
+  // 317 -> 322 outer it/s on the same box; at N = 64 it removes the bottleneck)
   if (!sb_off && p.gfast && p.btiles && p.fmode >= 0 && !p.ablate) {
     const int64_t If = p.g.dims[p.fmode];
     if (If % kTcRows == 0 && If / kTcRows >= 8) {

@@ -55,7 +55,7 @@ template <int N> __host__ __device__ constexpr int tc_bwarps() { return N > 32 ?
 template <int N> __host__ __device__ constexpr int tc_threads() { return 32 * (tc_bwarps<N>() + 7 + (tc_issuers<N>() - 1)); }
 constexpr int kTcBSbo = 272;    // bytes between 8-column groups of a B tile (256 + 16: bank spread)
 constexpr int kTcGModes = 3;    // factor modes gathered through the cp.async ring (more: direct fp64)
-constexpr size_t kTcSmemMax = 227 * 1024 - 6144;  // dynamic budget (static smem 5.4 KB + alignment slack)
+constexpr size_t kTcSmemMax = 227 * 1024 - 5120;  // dynamic budget (static smem 4.4 KB + 1 KB alignment slack)
 
 // runtime shared-memory layout (host-computed, tc_layout)
 struct TcLayout {
@@ -133,7 +133,10 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   __shared__ uint64_t g_full[kTcMaxGather], g_empty[kTcMaxGather];
   __shared__ uint32_t tmem_base;
   __shared__ double red[4][128];
-  __shared__ float gsm[2][128];  // static-B mode: run scale g per (stream, rank), double-buffered by segment
+  // static-B mode: run scale g per (stream, rank), double-buffered by segment.  Aliases the start of
+  // `red`: red is only touched in the per-item readout, which the drain groups' item barriers keep
+  // apart from every segment drain (the only readers/writers of gsm).
+  float (*gsm)[128] = reinterpret_cast<float (*)[128]>(&red[0][0]);
 
   // warp index through a shuffle: the compiler then treats the role branches
   // (and everything computed inside them from uniform inputs) as warp-uniform
