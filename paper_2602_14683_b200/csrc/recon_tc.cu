@@ -9,15 +9,22 @@
 
 namespace ntfg {
 
-template <int BK, int KC>
-static void launch_kc(int grid, cudaStream_t stream, const ReconParams<float>& p, int RP) {
+template <int BK, int KC, int HV>
+static void launch_hv(int grid, cudaStream_t stream, const ReconParams<float>& p, int RP) {
   static std::once_flag once;
   std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(recon_tc_kernel<BK, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cuda_check(cudaFuncSetAttribute(recon_tc_kernel<BK, KC, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(rc_smem(64))),
                "cudaFuncSetAttribute");
   });
-  recon_tc_kernel<BK, KC><<<grid, kRcThreads, rc_smem(RP), stream>>>(p, RP);
+  recon_tc_kernel<BK, KC, HV><<<grid, kRcThreads, rc_smem(RP), stream>>>(p, RP);
+}
+
+template <int BK, int KC>
+static void launch_kc(int grid, cudaStream_t stream, const ReconParams<float>& p, int RP) {
+  if ((p.R & 3) != 0) launch_hv<BK, KC, 0>(grid, stream, p, RP);
+  else if (p.hfac32 && !p.htab) launch_hv<BK, KC, 2>(grid, stream, p, RP);
+  else launch_hv<BK, KC, 1>(grid, stream, p, RP);
 }
 
 template <int BK>

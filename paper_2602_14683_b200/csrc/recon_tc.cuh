@@ -82,7 +82,11 @@ __device__ __forceinline__ void sts_b32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(a), "r"(v) : "memory");
 }
 
-template <int BK, int KC>
+// HV: H source of the producers -- 0 scalar fp64 (R % 4 != 0), 1 fp64 rows in 32-byte chunks,
+// 2 fp32 staged rows in 16-byte chunks.  A template parameter (like BK, KC) so an instance carries
+// one variant: this kernel is sensitive to its code size (a run-time choice between two split
+// routines in the unrolled epilogue cost 10%).
+template <int BK, int KC, int HV>
 static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const ReconParams<float> p, const int RP) {
   constexpr int64_t K = int64_t(KC) * kRcCols;
   extern __shared__ unsigned char smem_raw[];
@@ -191,7 +195,7 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
       // factor, or (Tucker partial chain) of the row table itself
       const double* hsrc = p.htab ? p.htab + row0 * R : p.fac[f] + p.g.coord(row0, f) * R;
       const uint32_t hhi = hbase + st * 2u * plane, hlo = hhi + plane;
-      if ((R & 3) == 0 && p.hfac32 && !p.htab) {
+      if constexpr (HV == 2) {
         // fp32 staged factor: one 16-byte load per item, fp32 product with the
         // (fp64-accumulated, then rounded) slower-mode product G
         const int R4 = R >> 2;
@@ -223,7 +227,7 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
             ++row;
           }
         }
-      } else if ((R & 3) == 0) {
+      } else if constexpr (HV == 1) {
         // four consecutive ranks of one row per item: 32-byte loads (a warp
         // reads 1 KB contiguous), one 16-byte store per plane (conflict-free
         // with the 144-byte core-matrix stride), one address per four values

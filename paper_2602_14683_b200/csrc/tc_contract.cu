@@ -10,15 +10,15 @@
 
 namespace ntfg {
 
-template <int N>
+template <int N, bool SB>
 static void launch_instance(int grid, cudaStream_t stream, const TcMaps& maps, const TcParams& p) {
   static std::once_flag once;
   std::call_once(once, [] {
-    cuda_check(cudaFuncSetAttribute(tc_contract_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cuda_check(cudaFuncSetAttribute(tc_contract_kernel<N, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(kTcSmemMax)),
                "cudaFuncSetAttribute");
   });
-  tc_contract_kernel<N><<<grid, tc_threads<N>(), p.lay.total, stream>>>(maps, p);
+  tc_contract_kernel<N, SB><<<grid, tc_threads<N>(), p.lay.total, stream>>>(maps, p);
 }
 
 // bf16 hi/lo B tiles of every 16-row block of the fastest off-mode's fp32 factor copy, in the
@@ -58,9 +58,15 @@ void tc_contract_launch(int grid, cudaStream_t stream, const TcMaps& maps, const
                                                                   p.ns, p.sb_runst, p.N, p.lay.b_tile, p.btiles);
     }
   }
-  if (p.N == 16) launch_instance<16>(grid, stream, maps, p);
-  else if (p.N == 32) launch_instance<32>(grid, stream, maps, p);
-  else launch_instance<64>(grid, stream, maps, p);
+  if (p.sb) {
+    if (p.N == 16) launch_instance<16, true>(grid, stream, maps, p);
+    else if (p.N == 32) launch_instance<32, true>(grid, stream, maps, p);
+    else launch_instance<64, true>(grid, stream, maps, p);
+  } else {
+    if (p.N == 16) launch_instance<16, false>(grid, stream, maps, p);
+    else if (p.N == 32) launch_instance<32, false>(grid, stream, maps, p);
+    else launch_instance<64, false>(grid, stream, maps, p);
+  }
 }
 
 }  // namespace ntfg

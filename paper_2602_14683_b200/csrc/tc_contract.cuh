@@ -122,7 +122,9 @@ __device__ __forceinline__ void bf16_split(double v, __nv_bfloat16& hi, __nv_bfl
 void tc_contract_launch(int grid, cudaStream_t stream, const TcMaps& maps, const TcParams& p);
 
 #ifdef NTFG_TC_CONTRACT_IMPL
-template <int NMAX>
+// SB: static-B mode (TcParams::sb) as a compile-time flag, so each instance carries only its own
+// roles' code (the generic producers / gather warp, or the TMA B copies and the drain groups)
+template <int NMAX, bool SB>
 static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     tc_contract_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   const TcLayout& L = p.lay;
@@ -211,7 +213,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
   // drain is ~1200 cycles of TMEM round trips, and the issuer cannot start a
   // tile's next segment before it is drained: draining the tiles in parallel
   // cut the issuer's wait from 14% of the launch.
-  const int ngroups = p.sb ? 1 + kB / 4 : 1;
+  const int ngroups = SB ? 1 + kB / 4 : 1;
   const int ntile_all = p.ns * p.mtw;
   const uint32_t cols_run = uint32_t(cols_per_buf);
   // one segment tile into the running sums: run = (sg ? run : 0) + seg * g
@@ -257,7 +259,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         const int blk0 = int(w % p.G) * 2 * p.mtw;  // first 64-column block of this item's m-tiles
         int64_t j0, j1, itgt, split;
         unit_range(u, j0, j1, itgt, split);
-        int rblk = p.sb ? int((j0 / kTcRows) % p.sb_runst) : 0;  // 16-row block of the fastest off-mode
+        int rblk = SB ? int((j0 / kTcRows) % p.sb_runst) : 0;  // 16-row block of the fastest off-mode
         for (int64_t j = j0; j < j1; j += kTcRows) {
           const unsigned long long tq = p.trace ? clock64() : 0;
           tc::wait(&empty[slot], sph);
@@ -270,11 +272,11 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
             c2 = int(j - aa * p.Bn); c3 = int(itgt); c4 = int(aa);
           }
           if (tc::elect_one()) {
-            tc::expect_tx(&a_full[slot], bytes + (p.sb ? unsigned(p.ns) * 2u * L.b_tile : 0u));
+            tc::expect_tx(&a_full[slot], bytes + (SB ? unsigned(p.ns) * 2u * L.b_tile : 0u));
             for (int s = 0; s < p.ns; ++s)
               for (int plane = 0; plane < 2; ++plane)
                 tc::tma_load_5d(stage_a(slot, s, plane), &maps.m[s][plane], 0, c2, c3, c4, blk0, &a_full[slot]);
-            if (p.sb)  // this stage's 16 factor rows as ready-made hi/lo B tiles (adjacent in smem)
+            if constexpr (SB)  // this stage's 16 factor rows as ready-made hi/lo B tiles (adjacent in smem)
               for (int s = 0; s < p.ns; ++s)
                 tma::bulk_g2s(stage_b(slot, s, 0), p.btiles + size_t((s * p.sb_runst + rblk) * 2) * L.b_tile,
                               2u * L.b_tile, &a_full[slot]);
@@ -324,13 +326,13 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
       unit_range(w / p.G, j0, j1, itgt, split);
       const int nstage = int((j1 - j0 + kTcRows - 1) / kTcRows);
       int qi = 0;
-      int rblk = p.sb ? int((j0 / kTcRows) % p.sb_runst) : 0;
+      int rblk = SB ? int((j0 / kTcRows) % p.sb_runst) : 0;
       for (int stg = 0; stg < nstage; ++stg) {
         const bool seg_first = qi == 0;
-        const bool seg_last = qi == p.seg - 1 || stg == nstage - 1 || (p.sb && rblk == p.sb_runst - 1);
+        const bool seg_last = qi == p.seg - 1 || stg == nstage - 1 || (SB && rblk == p.sb_runst - 1);
         if (++rblk == p.sb_runst) rblk = 0;
         tc::wait(&a_full[slot], sph);
-        if (!p.sb) tc::wait(&b_full[slot], sph);
+        if constexpr (!SB) tc::wait(&b_full[slot], sph);
         tc::fence_after_sync();
         for (int t = issuer; t < ntile; t += tc_issuers<NMAX>()) {
           const int s = t >= p.mtw ? 1 : 0, m = t - s * p.mtw;
@@ -369,7 +371,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         }
       }
     }
-    if (p.trace && p.sb && lane == 0 && issuer == 0) p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 2] = iw;
+    if (p.trace && SB && lane == 0 && issuer == 0) p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 2] = iw;
   } else if (warp == kWGather) {
     // ================= factor-row gathers (bulk async copies) =================
     // gather slot q % gdepth holds, per stream, gm regions of [16][N] floats.
@@ -394,7 +396,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     int gs = 0;
     uint32_t gph = 1;  // producer parity: the first pass finds every gather slot free
     unsigned long long gw = 0, g00 = p.trace ? clock64() : 0;
-    if (gm > 0 && !(p.ablate & 1) && !p.sb) {
+    if constexpr (!SB) if (gm > 0 && !(p.ablate & 1)) {
       for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
         int64_t j0, j1, itgt, split;
         unit_range(w / p.G, j0, j1, itgt, split);
@@ -457,7 +459,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     int slot = -1, gs = -1;           // ring positions (advanced at the top of every stage)
     uint32_t sph = 0, gph = 1;        // sph: parity the slot's "empty" wait uses (ph ^ 1 trick); gph: gather "full" parity
     unsigned long long bw0 = 0, bw1 = 0, b00 = p.trace ? clock64() : 0;
-    for (int64_t w = blockIdx.x; w < p.items && !p.sb; w += gridDim.x) {
+    if constexpr (!SB) for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
       int64_t j0, j1, itgt, split;
       unit_range(w / p.G, j0, j1, itgt, split);
       for (int64_t jb = j0; jb < j1; jb += kTcRows) {
@@ -541,7 +543,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         tc::warp_arrive(&b_full[slot], lane);
       }
     }
-    if (p.sb) {
+    if constexpr (SB) {
       // ---- helper drain group (see drain_tile): warps 4q .. 4q+3 are group q + 1
       const int grp = 1 + warp / 4;
       const uint32_t lanes_ = uint32_t((warp & 3) * 32) << 16;
@@ -584,7 +586,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         tc::fence_after_sync();
       }
     }
-    if (p.trace && !p.sb && tid == 0) {
+    if (p.trace && !SB && tid == 0) {
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 0] = bw0;
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 1] = bw1;
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 2] = clock64() - b00;
@@ -611,7 +613,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     int nom = 0;  // off-modes other than the fastest one
     for (int m = 0; m < nrm; ++m)
       if (m != p.n && m != p.fmode) om[nom++] = m;
-    const bool has_g = p.sb && nom > 0;
+    const bool has_g = SB && nom > 0;
     auto g_of = [&](int64_t j, int64_t itgt) -> float {
       if (!has_g || et >= p.ns * N) return 1.f;
       const int s = et / N, r = et - s * N;
@@ -629,10 +631,10 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
       unit_range(u, j0, j1, itgt, split);
       const int nstage = int((j1 - j0 + kTcRows - 1) / kTcRows);
       int qi = 0, sg = 0;
-      int rblk = p.sb ? int((j0 / kTcRows) % p.sb_runst) : 0;
+      int rblk = SB ? int((j0 / kTcRows) % p.sb_runst) : 0;
       float gnext = g_of(j0, itgt);
       for (int stg = 0; stg < nstage; ++stg) {
-        const bool seg_last = qi == p.seg - 1 || stg == nstage - 1 || (p.sb && rblk == p.sb_runst - 1);
+        const bool seg_last = qi == p.seg - 1 || stg == nstage - 1 || (SB && rblk == p.sb_runst - 1);
         if (++rblk == p.sb_runst) rblk = 0;
         if (!seg_last) {
           ++qi;
@@ -749,7 +751,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
       }
     }
   }
-  if (p.trace && p.sb && tid == kB * 32) {  // static-B mode: the B counters' slots carry the epilogue's
+  if (p.trace && SB && tid == kB * 32) {  // static-B mode: the B counters' slots carry the epilogue's
     p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 0] = ew_out;
     p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 1] = ed_out;
   }
