@@ -27,6 +27,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xcompiler", "-fvisibility=hidden", "-I" + INCLUDE, "-I" + CSRC]
+if os.environ.get("NTFG_TC_TRACE_BUILD") == "1":  # role wait counters of tc_contract_kernel (tools/tc_wstats.py)
+    NVFLAGS = NVFLAGS + ["-DNTFG_TC_TRACE_BUILD"]
 CU_SOURCES = ["cp_api.cu", "tucker_api.cu", "io_api.cu", "unfold_api.cu", "capi.cu", "tc_contract.cu", "recon_tc.cu"]
 CXX_API_SOURCES = ["ntf_api.cpp"]
 

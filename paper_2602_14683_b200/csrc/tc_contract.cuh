@@ -127,6 +127,13 @@ void tc_contract_launch(int grid, cudaStream_t stream, const TcMaps& maps, const
 template <int NMAX, bool SB>
 static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     tc_contract_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
+  // role wait counters (tools/tc_wstats.py): compiled in only with -DNTFG_TC_TRACE_BUILD, the
+  // kernel is sensitive to its code size
+#ifdef NTFG_TC_TRACE_BUILD
+  const bool kTrace = p.trace != nullptr;
+#else
+  constexpr bool kTrace = false;
+#endif
   const TcLayout& L = p.lay;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -253,7 +260,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
       int slot = 0;
       uint32_t sph = 1;  // producer parity: the first pass over the ring finds every slot free
       const unsigned bytes = unsigned(p.ns) * 2u * unsigned(2 * p.mtw) * 2048u;
-      unsigned long long tw = 0, t00 = p.trace ? clock64() : 0;
+      unsigned long long tw = 0, t00 = kTrace ? clock64() : 0;
       for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
         const int64_t u = w / p.G;
         const int blk0 = int(w % p.G) * 2 * p.mtw;  // first 64-column block of this item's m-tiles
@@ -261,9 +268,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         unit_range(u, j0, j1, itgt, split);
         int rblk = SB ? int((j0 / kTcRows) % p.sb_runst) : 0;  // 16-row block of the fastest off-mode
         for (int64_t j = j0; j < j1; j += kTcRows) {
-          const unsigned long long tq = p.trace ? clock64() : 0;
+          const unsigned long long tq = kTrace ? clock64() : 0;
           tc::wait(&empty[slot], sph);
-          if (p.trace) tw += clock64() - tq;
+          if (kTrace) tw += clock64() - tq;
           int c2, c3, c4;
           if (p.caseA) {
             c2 = int(j); c3 = 0; c4 = 0;
@@ -289,7 +296,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
           }
         }
       }
-      if (p.trace && lane == 0) {
+      if (kTrace && lane == 0) {
         p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 5] = tw;
         p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 6] = clock64() - t00;
       }
@@ -337,9 +344,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         for (int t = issuer; t < ntile; t += tc_issuers<NMAX>()) {
           const int s = t >= p.mtw ? 1 : 0, m = t - s * p.mtw;
           if (seg_first) {  // the epilogue drained this tile's previous segment
-            const unsigned long long tq = p.trace ? clock64() : 0;
+            const unsigned long long tq = kTrace ? clock64() : 0;
             tc::wait(&acc_empty[t], (sc & 1u) ^ 1u);
-            if (p.trace) iw += clock64() - tq;
+            if (kTrace) iw += clock64() - tq;
             tc::fence_after_sync();
           }
           const uint32_t aoff = uint32_t(slot) * L.a_stage + uint32_t(s) * L.a_stream + uint32_t(m) * 4096u;
@@ -371,7 +378,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         }
       }
     }
-    if (p.trace && SB && lane == 0 && issuer == 0) p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 2] = iw;
+    if (kTrace && SB && lane == 0 && issuer == 0) p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 2] = iw;
   } else if (warp == kWGather) {
     // ================= factor-row gathers (bulk async copies) =================
     // gather slot q % gdepth holds, per stream, gm regions of [16][N] floats.
@@ -395,15 +402,15 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     unsigned char* ring = smem + L.ring_off;
     int gs = 0;
     uint32_t gph = 1;  // producer parity: the first pass finds every gather slot free
-    unsigned long long gw = 0, g00 = p.trace ? clock64() : 0;
+    unsigned long long gw = 0, g00 = kTrace ? clock64() : 0;
     if constexpr (!SB) if (gm > 0 && !(p.ablate & 1)) {
       for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
         int64_t j0, j1, itgt, split;
         unit_range(w / p.G, j0, j1, itgt, split);
         for (int64_t jb = j0; jb < j1; jb += kTcRows) {
-          const unsigned long long tq = p.trace ? clock64() : 0;
+          const unsigned long long tq = kTrace ? clock64() : 0;
           tc::wait(&g_empty[gs], gph);
-          if (p.trace) gw += clock64() - tq;
+          if (kTrace) gw += clock64() - tq;
           if (lane == 0) tc::expect_tx(&g_full[gs], bytes);
           __syncwarp();
           if (p.gfast) {
@@ -434,7 +441,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         }
       }
     }
-    if (p.trace && lane == 0) {
+    if (kTrace && lane == 0) {
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 3] = gw;
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 4] = clock64() - g00;
     }
@@ -458,7 +465,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
     constexpr int kMaxItems = (4 * N + kBT - 1) / kBT;            // ns * 2 * N items per stage
     int slot = -1, gs = -1;           // ring positions (advanced at the top of every stage)
     uint32_t sph = 0, gph = 1;        // sph: parity the slot's "empty" wait uses (ph ^ 1 trick); gph: gather "full" parity
-    unsigned long long bw0 = 0, bw1 = 0, b00 = p.trace ? clock64() : 0;
+    unsigned long long bw0 = 0, bw1 = 0, b00 = kTrace ? clock64() : 0;
     if constexpr (!SB) for (int64_t w = blockIdx.x; w < p.items; w += gridDim.x) {
       int64_t j0, j1, itgt, split;
       unit_range(w / p.G, j0, j1, itgt, split);
@@ -473,9 +480,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
           continue;
         }
         const int nvalid = int(j1 - jb < kTcRows ? j1 - jb : kTcRows);
-        unsigned long long tq = p.trace ? clock64() : 0;
+        unsigned long long tq = kTrace ? clock64() : 0;
         if (gm > 0) tc::wait(&g_full[gs], gph);
-        if (p.trace) { bw0 += clock64() - tq; }
+        if (kTrace) { bw0 += clock64() - tq; }
         uint4 hv[kMaxItems], lv[kMaxItems];
 #pragma unroll
         for (int it = 0; it < kMaxItems; ++it) {
@@ -526,9 +533,9 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
           lv[it] = make_uint4(l[0], l[1], l[2], l[3]);
         }
         if (gm > 0) tc::warp_arrive(&g_empty[gs], lane);
-        tq = p.trace ? clock64() : 0;
+        tq = kTrace ? clock64() : 0;
         tc::wait(&empty[slot], sph);
-        if (p.trace) { bw1 += clock64() - tq; }
+        if (kTrace) { bw1 += clock64() - tq; }
 #pragma unroll
         for (int it = 0; it < kMaxItems; ++it) {
           const int i = tid + it * kBT;
@@ -586,7 +593,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
         tc::fence_after_sync();
       }
     }
-    if (p.trace && !SB && tid == 0) {
+    if (kTrace && !SB && tid == 0) {
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 0] = bw0;
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 1] = bw1;
       p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 2] = clock64() - b00;
@@ -648,10 +655,10 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
           named_sync(ngroups > 1 ? 3 : 1, 128 * ngroups);
         }
         for (int t = 0; t < ntile; t += ngroups) {
-          const unsigned long long tq0 = p.trace ? clock64() : 0;
+          const unsigned long long tq0 = kTrace ? clock64() : 0;
           tc::wait(&acc_full[t], sc & 1u);
           tc::fence_after_sync();
-          if (p.trace) {
+          if (kTrace) {
             const unsigned long long tq1 = clock64();
             ew += tq1 - tq0;
             ed -= tq1;
@@ -659,7 +666,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
           if (!(p.ablate & 4)) drain_tile(t, sg == 0, has_g, gcur, lanes);
           tc::fence_before_sync();
           tc::warp_arrive(&acc_empty[t], lane);  // the segment tile is read: its next segment may start
-          if (p.trace) ed += clock64();
+          if (kTrace) ed += clock64();
         }
         tc::tmem_st_wait();
         ew_out = ew;
@@ -751,7 +758,7 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
       }
     }
   }
-  if (p.trace && SB && tid == kB * 32) {  // static-B mode: the B counters' slots carry the epilogue's
+  if (kTrace && SB && tid == kB * 32) {  // static-B mode: the B counters' slots carry the epilogue's
     p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 0] = ew_out;
     p.trace[size_t(gridDim.x) * 128 + blockIdx.x * 8 + 1] = ed_out;
   }

@@ -1,5 +1,7 @@
 """Per-launch medians of the role wait counters of tc_contract_kernel (NTFG_TC_TRACE file):
 B producers (wait gathers / wait slot / total), gather warp (wait / total), TMA producer (wait / total), in cycles.
+The counters are compiled in only by a trace build:
+  NTFG_TC_TRACE_BUILD=1 python -c "from paper_2602_14683_b200 import build as B; B.build(force=True)"
 usage: NTFG_TC_TRACE=/tmp/t.txt python tools/prof_c5.py 1; python tools/tc_wstats.py /tmp/t.txt"""
 import statistics as S
 import sys
