@@ -14,10 +14,10 @@ static void launch_hv(int grid, cudaStream_t stream, const ReconParams<float>& p
   static std::once_flag once;
   std::call_once(once, [] {
     cuda_check(cudaFuncSetAttribute(recon_tc_kernel<BK, KC, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(rc_smem(64))),
+                                    int(232448 - 1536)),
                "cudaFuncSetAttribute");
   });
-  recon_tc_kernel<BK, KC, HV><<<grid, kRcThreads, rc_smem(RP), stream>>>(p, RP);
+  recon_tc_kernel<BK, KC, HV><<<grid, kRcThreads, rc_smem(RP), stream>>>(p, RP, rc_stages(RP));
 }
 
 template <int BK, int KC>

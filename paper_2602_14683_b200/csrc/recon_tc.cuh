@@ -52,7 +52,15 @@ constexpr int kRcLbo = 144;
 
 __host__ __device__ inline uint32_t rc_sbo(int RP) { return uint32_t(RP / 4) * kRcLbo; }      // between 8-row groups
 __host__ __device__ inline uint32_t rc_plane(int RP) { return 16u * rc_sbo(RP); }             // one 128 x RP tf32 plane
-inline size_t rc_smem(int RP) { return size_t(6) * rc_plane(RP) + 128; }  // A hi/lo + 2 stages of H hi/lo
+constexpr int kRcMaxStages = 4;
+// H stages (2..4) that fit next to the A planes: 2 at R = 64, 4 below (a deeper ring absorbs the
+// producers' latency jitter; the accumulator stays double-buffered)
+inline int rc_stages(int RP) {
+  const int planes = int((size_t(232448) - 1536 - 128) / rc_plane(RP));
+  const int nh = (planes - 2) / 2;
+  return nh < 2 ? 2 : nh > kRcMaxStages ? kRcMaxStages : nh;
+}
+inline size_t rc_smem(int RP) { return size_t(2 + 2 * rc_stages(RP)) * rc_plane(RP) + 128; }  // A hi/lo + NH stages of H hi/lo
 
 // the launcher lives in recon_tc.cu (own translation unit)
 void recon_tc_launch(int grid, cudaStream_t stream, const ReconParams<float>& p, int RP, int bk);
@@ -87,11 +95,12 @@ __device__ __forceinline__ void sts_b32(uint32_t a, uint32_t v) {
 // one variant: this kernel is sensitive to its code size (a run-time choice between two split
 // routines in the unrolled epilogue cost 10%).
 template <int BK, int KC, int HV>
-static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const ReconParams<float> p, const int RP) {
+static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const ReconParams<float> p, const int RP,
+                                                                        const int NH) {
   constexpr int64_t K = int64_t(KC) * kRcCols;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  __shared__ uint64_t h_full[2], h_empty[2], acc_full[2], acc_empty[2];
+  __shared__ uint64_t h_full[kRcMaxStages], h_empty[kRcMaxStages], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(16) double gs[2][64];
   __shared__ double red[kRcEpiWarps];
@@ -107,9 +116,11 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
   const int64_t tile0 = blockIdx.x / KC;
 
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kRcMaxStages; ++b) {
       tc::mbar_init(&h_full[b], kRcProdWarps);  // one arrival per warp
       tc::mbar_init(&h_empty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&acc_full[b], 1);
       tc::mbar_init(&acc_empty[b], kRcEpiWarps);
     }
@@ -132,7 +143,7 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
       sts_b32(a_lo + off, lo);
     }
     uint4* hz = reinterpret_cast<uint4*>(smem + 2 * size_t(plane));
-    for (int i = tid; i < int(4 * plane / 16); i += kRcThreads) hz[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < int(2 * NH * plane / 16); i += kRcThreads) hz[i] = make_uint4(0u, 0u, 0u, 0u);
     tc::fence_proxy_async();
   }
   tc::fence_before_sync();
@@ -151,12 +162,14 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
     const uint64_t h0 = tc::desc_k_interleave(smem + 2 * size_t(plane), kRcLbo, sbo);
     const int ksteps = RP / 8;
     uint32_t i = 0;
+    int hs = 0;        // H stage ring position / parity
+    uint32_t hph = 0;
     for (int64_t tile = tile0; tile < ntiles; tile += tstride, ++i) {
-      const uint32_t st = i & 1u, ph = (i >> 1) & 1u;
-      tc::wait(&h_full[st], ph);
+      const uint32_t st = i & 1u, ph = (i >> 1) & 1u;  // accumulator buffer / parity
+      tc::wait(&h_full[hs], hph);
       tc::wait(&acc_empty[st], ph ^ 1u);
       tc::fence_after_sync();
-      const uint64_t b_hi = h0 + uint64_t(st) * (2u * plane >> 4);
+      const uint64_t b_hi = h0 + uint64_t(hs) * (2u * plane >> 4);
       const uint64_t b_lo = b_hi + (plane >> 4);
       const uint32_t d = tmem + st * uint32_t(kRcRows);
       if (tc::elect_one()) {
@@ -166,10 +179,14 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
           mma_tf32(d, a_hi + ko, b_lo + ko, idesc, true);
           mma_tf32(d, a_lo + ko, b_hi + ko, idesc, true);
         }
-        tc::commit(&h_empty[st]);
+        tc::commit(&h_empty[hs]);
         tc::commit(&acc_full[st]);
       }
       __syncwarp();
+      if (++hs == NH) {
+        hs = 0;
+        hph ^= 1u;
+      }
     }
   } else if (warp >= kRcEpiWarps) {
     // ================= H producers =================
@@ -181,9 +198,11 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
     const int nel = kRcRows * R;
     const uint32_t hbase = tc::saddr(smem) + 2u * plane;
     uint32_t i = 0;
+    int hs = 0;
+    uint32_t hph = 1;  // producer parity: the first pass over the ring finds every stage free
     for (int64_t tile = tile0; tile < ntiles; tile += tstride, ++i) {
-      const uint32_t st = i & 1u;
-      tc::wait(&h_empty[st], ((i >> 1) & 1u) ^ 1u);
+      const uint32_t st = i & 1u;  // G buffer (guarded by the per-tile producer barrier)
+      tc::wait(&h_empty[hs], hph);
       const int64_t row0 = tile * kRcRows;
       if (npre >= 2 && pt < R) {  // product of the slower modes' rows, reference order
         double g = p.fac[0][p.g.coord(row0, 0) * R + pt];
@@ -194,7 +213,7 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
       // H rows of the tile: 128 consecutive rows of the fastest row mode's
       // factor, or (Tucker partial chain) of the row table itself
       const double* hsrc = p.htab ? p.htab + row0 * R : p.fac[f] + p.g.coord(row0, f) * R;
-      const uint32_t hhi = hbase + st * 2u * plane, hlo = hhi + plane;
+      const uint32_t hhi = hbase + uint32_t(hs) * 2u * plane, hlo = hhi + plane;
       if constexpr (HV == 2) {
         // fp32 staged factor: one 16-byte load per item, fp32 product with the
         // (fp64-accumulated, then rounded) slower-mode product G
@@ -282,7 +301,11 @@ static __global__ void __launch_bounds__(kRcThreads, 1) recon_tc_kernel(const Re
         }
       }
       tc::fence_proxy_async();
-      tc::warp_arrive(&h_full[st], lane);
+      tc::warp_arrive(&h_full[hs], lane);
+      if (++hs == NH) {
+        hs = 0;
+        hph ^= 1u;
+      }
     }
   } else {
     // ================= epilogue =================
