@@ -77,6 +77,8 @@ class CpEngine {
     colprod_ = c_.buf<double>("cp.colprod", size_t(R_));
     flags_ = c_.buf<unsigned>("cp.flags", 1);
     counter_ = c_.buf<int>("cp.counter", 1);
+    colsum_done_ = c_.buf<int>("cp.colsum_done", 1);
+    NTFG_CUDA(cudaMemsetAsync(colsum_done_, 0, sizeof(int), c_.stream));
     raw_ = c_.buf<double>("cp.raw", 1);
     numden_ = c_.buf<double>("cp.numden", size_t(2) * max_dim() * R_);
     // objective partials: one per recon CTA (grid depends on the kernel variant)
@@ -748,11 +750,18 @@ class CpEngine {
       p.fac[m] = fac[m];
     }
     p.out = colsum_;
+    // two launches when the slab-local mode-0 column sums are allreduced in between, or when no
+    // block takes part (order-1 tensors: the empty product)
+    const bool split = (sharded_ && skip != 0) || N_ - ((skip >= 0 && skip < N_) ? 1 : 0) == 0;
+    p.prod = split ? nullptr : colprod_;
+    p.done = colsum_done_;
     colsum_kernel<<<N_, kColsumThreads, 0, c_.stream>>>(p);
     NTFG_LAUNCHED(c_);
-    if (sharded_ && skip != 0) allreduce(colsum_, size_t(R_));  // slab-local mode-0 colsum
-    colprod_kernel<<<int(ceil_div(R_, 64)), 64, 0, c_.stream>>>(colsum_, N_, skip, int(R_), colprod_);
-    NTFG_LAUNCHED(c_);
+    if (split) {
+      allreduce(colsum_, size_t(R_));
+      colprod_kernel<<<int(ceil_div(R_, 64)), 64, 0, c_.stream>>>(colsum_, N_, skip, int(R_), colprod_);
+      NTFG_LAUNCHED(c_);
+    }
   }
 
   // ---- solver steps ----------------------------------------------------------------------
@@ -1449,6 +1458,7 @@ class CpEngine {
   float* hstage_ = nullptr;   // fp32 copy of the fastest row mode's factor (recon_tc H producers)
   unsigned* flags_;
   int* counter_;
+  int* colsum_done_;  // arrival counter of the fused colsum + colprod launch (self re-arming)
   int recon_grid_ = 0;
   bool recon_v3_ = false;
   bool obj_split_ = false;    // last recon used the split objective (needs xconst_)

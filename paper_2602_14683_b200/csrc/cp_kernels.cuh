@@ -238,6 +238,10 @@ struct ColsumParams {
   int64_t rows[kMaxOrder];
   const double* fac[kMaxOrder];
   double* out;
+  // fused closed-form denominator (nullable): the last block to finish writes
+  // prod[r] = prod_{m != skip} out[m][r] (ascending m) and re-arms the counter
+  double* prod;
+  int* done;
 };
 
 // column sums of every factor but `skip`, one 1024-thread block per mode:
@@ -277,6 +281,29 @@ static __global__ void __launch_bounds__(kColsumThreads) colsum_kernel(const Col
       p.out[m * R + r0 + t] = tot;
     }
     __syncthreads();
+  }
+  if (p.prod) {
+    // one launch instead of two per beta = 1 block update: the block that
+    // completes the set of column sums forms the product (fixed order, from the
+    // values every block published before its arrival)
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (t == 0) {
+      const int parts = p.order - ((p.skip >= 0 && p.skip < p.order) ? 1 : 0);
+      last = atomicAdd(p.done, 1) == parts - 1;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      for (int r = t; r < R; r += kColsumThreads) {
+        double prod = 1.0;
+        for (int mm = 0; mm < p.order; ++mm)
+          if (mm != p.skip) prod *= __ldcg(p.out + mm * R + r);
+        p.prod[r] = prod;
+      }
+      if (t == 0) *p.done = 0;
+    }
   }
 }
 
