@@ -2,8 +2,7 @@
 //   G(k, r) = sum_{rows of unit} S(row, k) M(row, r)
 // as a UMMA with A = S^T (M-dim = 128 columns k, K-dim = 16 rows, MN-major,
 // TMA-loaded with the 128-byte swizzle straight from the row-major data),
-// B = M (K-dim = 16 rows, N = rank, K-major, written by producer warps) and
-// the fp32 accumulator in TMEM.
+// B = M (K-dim = 16 rows, N = rank, K-major) and the fp32 accumulator in TMEM.
 //
 // Precision: the weight tensors P~/Q~ are stored by the reconstruction pass
 // as two bf16 planes (hi = bf16(p), lo = bf16(p - hi), ~2^-17 relative) and
@@ -12,24 +11,35 @@
 // cross-unit reductions stay fp64 (hard part 2).  Same 8 bytes
 // per entry per pass as fp32 P~/Q~.
 //
-// Warp roles (352 threads): 0-3 build the B tiles (M rows), 4-7 epilogue
-// (tcgen05.ld -> partials), 8 TMA producer, 9 TMEM allocator + single-thread
-// MMA issuer (+ warp 11: second issuer), 10 factor-row gathers.  Stages of 16 rows cycle through a smem ring (2-6 deep, sized
-// from K at launch) guarded by mbarriers (TMA tx, B-tile arrivals,
-// tcgen05.commit); the TMEM accumulator is double-buffered across units when
-// it fits so the epilogue of one unit overlaps the next.
+// Two instances per rank width N (template flag SB):
 //
-// B producers: each thread owns one stage row and W = N/8 rank columns.  The
-// factor rows it multiplies come from fp32 zero-padded copies of the factors
-// (stage_f32_kernel, one launch per contraction), gathered by warp 10 with
-// bulk async copies (async proxy, mbarrier completion) into a smem ring
-// `gdepth` stages ahead of the MMA.  Keeping the gathers out of the B threads
-// matters twice: their L2 latency leaves the stage cadence, and the B
-// threads' per-stage fence.proxy.async no longer waits for in-flight loads
-// (register or cp.async gathers in the B threads made a K = 256 / R = 64
-// stage take ~3 us -- 23% of HBM -- on C5).  B tiles use a 272-byte stride between
-// 8-column core-matrix groups (SBO) so the 2-byte stores of one warp hit 16
-// distinct banks instead of 2.
+// * SB = true, static B tiles (fast shapes: the fastest off-mode f has 128 | I_f).
+//   M(row, r) = g(r) * A_f(c_f, r), with g (the slower off-modes' rows) constant
+//   over a run of I_f rows.  The B operand of a stage is the bf16 hi/lo split of
+//   16 rows of A_f alone, built once per launch in global memory in the tile
+//   layout (stage_btiles_kernel) and bulk-copied per stage by the TMA warp; g
+//   scales each finished accumulation segment in the epilogue (segments end at
+//   run boundaries).  No per-stage producer work.
+// * SB = false, generic: producer warps multiply the fp32 factor rows a gather
+//   warp fetched with bulk async copies (`gdepth` stages ahead) and write the
+//   hi/lo tiles per stage (272-byte stride between 8-column core-matrix groups,
+//   so a warp's stores are conflict-free).
+//
+// Warp roles: [0, kB) B producers (SB: extra drain groups), kB..kB+3 epilogue
+// (TMEM lane quarter = warp % 4), then TMA producer, MMA issuer (+ TMEM
+// allocator), gather warp, second issuer (N <= 32).  The TMA and MMA warps run
+// converged with warp-uniform operands and an elected lane (a single divergent
+// issuing lane costs 150-350 cycles per MMA in compiler-generated operand
+// marshalling, tools/mma_probe.cu).  Stages of 16 rows cycle through a smem
+// ring (3-6 deep by budget) guarded by mbarriers (TMA tx, B arrivals,
+// tcgen05.commit).
+//
+// Accumulation is segmented: a tile's TMEM accumulator restarts every p.seg
+// stages and the epilogue adds the finished segment into running sums in a
+// second TMEM region with CUDA-core FMAs -- long fp32 chains inside the tensor
+// core truncate and drift (see the issuer).  One segment buffer, per-tile
+// full/empty barriers; in SB mode the tiles of a segment are drained by
+// several warp groups in parallel.
 #pragma once
 #include <cuda_bf16.h>
 
