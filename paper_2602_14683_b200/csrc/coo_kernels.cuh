@@ -148,7 +148,7 @@ static __global__ void __launch_bounds__(kCooWarps * 32) coo_piece2_kernel(const
         const double x = p.val[jb + lane];
         double y = 0.0;
         if (vec) {
-#pragma unroll 2
+#pragma unroll 5
           for (int r = 0; r < R; r += 2) {
             double2 a = __ldg(reinterpret_cast<const double2*>(row[0] + r));
 #pragma unroll
@@ -176,6 +176,7 @@ static __global__ void __launch_bounds__(kCooWarps * 32) coo_piece2_kernel(const
         pj[lane] = x / c;                        // weight_entries beta = 1 (kernels.hpp)
         if (p.partial) {
           double* orow = off + size_t(lane) * RS;
+#pragma unroll 4
           for (int r = 0; r < R; ++r) {
             double o = 1.0;
 #pragma unroll
