@@ -518,8 +518,6 @@ class CpEngine {
                                 p.boxA, 2 * p.mtw))
           throw Error(NTFG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     }
-    stage_f32_kernel<<<int(std::min<int64_t>(ceil_div(fs.off[N_] * ns, 256), 1024)), 256, 0, c_.stream>>>(fs);
-    NTFG_LAUNCHED(c_);
     int nmm = 0;
     for (int m = 0; m < N_ - 1; ++m) nmm += (m != n);
     {  // fast gathers: the fastest off-mode f (highest index != n among the row modes) has 16 | I_f
@@ -550,7 +548,8 @@ class CpEngine {
       p.trace = reinterpret_cast<unsigned long long*>(c_.bufs.get("cp.tctrace", size_t(grid) * 17 * 8 * 8));
       NTFG_CUDA(cudaMemsetAsync(p.trace, 0, size_t(grid) * 17 * 8 * 8, c_.stream));
     }
-    tc_contract_launch(grid, c_.stream, maps, p);
+    tc_contract_launch(grid, c_.stream, maps, p, fs);  // staging launch + contraction
+    NTFG_LAUNCHED(c_);
     NTFG_LAUNCHED(c_);
     if (trace_path) {
       std::vector<unsigned long long> h(size_t(grid) * 17 * 8);

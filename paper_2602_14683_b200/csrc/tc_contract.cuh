@@ -126,10 +126,19 @@ __device__ __forceinline__ void bf16_split(double v, __nv_bfloat16& hi, __nv_bfl
   lo = __float2bfloat16_rn(f - __bfloat162float(hi));
 }
 
+// every factor of every stream, [I_m][R] fp64 -> [I_m][N] fp32 zero padded:
+// the B-operand gathers and the case-B epilogue's last factor (16-byte loads)
+struct F32Stage {
+  const double* src[2][kMaxOrder];
+  float* dst[2][kMaxOrder];
+  int64_t off[kMaxOrder + 1];  // cumulative I_m * N
+  int order, ns, R, N;
+};
+
 // The kernel lives in its own translation unit (tc_contract.cu); the engine
-// launches it through this entry point (sets the dynamic shared-memory
-// attribute once per instance).
-void tc_contract_launch(int grid, cudaStream_t stream, const TcMaps& maps, const TcParams& p);
+// launches it through this entry point: ONE staging launch (fp32 factor copies
+// and, in static-B mode, the B tiles), then the contraction.
+void tc_contract_launch(int grid, cudaStream_t stream, const TcMaps& maps, const TcParams& p, const F32Stage& fs);
 
 #ifdef NTFG_TC_CONTRACT_IMPL
 // SB: static-B mode (TcParams::sb) as a compile-time flag, so each instance carries only its own
@@ -778,29 +787,6 @@ static __global__ void __launch_bounds__(tc_threads<NMAX>(), 1)
 }
 
 #endif  // NTFG_TC_CONTRACT_IMPL
-
-// every factor of every stream, [I_m][R] fp64 -> [I_m][N] fp32 zero padded:
-// the B-operand gathers and the case-B epilogue's last factor (16-byte loads)
-struct F32Stage {
-  const double* src[2][kMaxOrder];
-  float* dst[2][kMaxOrder];
-  int64_t off[kMaxOrder + 1];  // cumulative I_m * N
-  int order, ns, R, N;
-};
-static __global__ void stage_f32_kernel(const F32Stage a) {
-  const int64_t tot = a.off[a.order];
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < tot * a.ns;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int s = int(i / tot);
-    const int64_t e = i - s * tot;
-    int m = 0;
-    while (e >= a.off[m + 1]) ++m;
-    const int64_t l = e - a.off[m];
-    const int64_t row = l / a.N;
-    const int r = int(l - row * a.N);
-    a.dst[s][m][l] = r < a.R ? float(a.src[s][m][row * a.R + r]) : 0.f;
-  }
-}
 
 // host P~/Q~ (fp64) -> bf16 hi/lo planes (step-level uploads).  The split is
 // done in fp64 so that values produced as hi + lo by join_planes_kernel map
